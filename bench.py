@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark: the FullSWOF_2D explicit time step (one Heun step = one "step") on cfg4 (8192 x 8192, the
+BASELINE.json throughput/roofline configuration), fp64, 1 x B200 per rank.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg4]
+
+N > 1 is launched by torchrun; every rank advances its own full cfg4 replica (the north star excludes
+domain decomposition: "replicas only", weak scaling, no data-path collective).  Timing: W untimed
+steps, then exactly K steps bracketed by barrier + cuda synchronize, CUDA events on the context's
+stream, max over ranks.  The inputs (4.6 GB of fields) are far larger than the 126 MB L2, so no flush
+is needed between steps.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/sec (fp64, 1xB200)"
+UNIT = "cell-updates/s"
+
+# Algorithmic fp64 operations of the canonical sheet, each add/sub/mul/div/sqrt/min/max/abs/
+# cube-root = 1: per cell and stage, per face by HLL branch, per cell and step.
+OPS_CELL_STAGE = 4 + 64 + 28 + 1          # primitives, MUSCL (2 axes), update (2 axes), rain
+OPS_GA = 10
+OPS_FRIC_WET = {"manning": 13, "strickler": 13, "darcy_weisbach": 12, "chezy": 12}
+OPS_FIELD = 3                               # g*(n*n), dt*gc per cell with a per-cell coefficient field
+OPS_FACE = {"dry": 15, "left": 39, "right": 39, "mid": 63}
+OPS_STEP = 8 + 11                           # Heun (with V), CFL speeds + max
+# algorithmic DRAM bytes per cell-update of the per-stage design: predictor reads
+# h,hu,hv,z (+V, +n) and writes h,hu,hv (+V); corrector reads U* and z (+V*, +n), U^n (+V^n), writes U^{n+1} (+V)
+def bytes_per_cell_update(ga: bool, field: bool):
+    pred = 8 * (4 + ga + field) + 8 * (3 + ga)
+    corr = 8 * (4 + ga + field) + 8 * (3 + ga) + 8 * (3 + ga)
+    return pred, corr
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def cpu_sample(cfg, crop: int, steps: int):
+    """The oracle, as it stands, on a crop x crop window of the workload: (cell-updates/s, counters, secs)."""
+    import oracle
+    from workloads.configs import SwofConfig
+    j0 = (cfg.ny - crop) // 2
+    i0 = (cfg.nx - crop) // 2
+    sl = (slice(j0, j0 + crop), slice(i0, i0 + crop))
+    sub = SwofConfig(**{**cfg.__dict__, "nx": crop, "ny": crop})
+    for k in ("z", "h", "hu", "hv", "vinf", "fric_field"):
+        a = getattr(cfg, k)
+        setattr(sub, k, None if a is None else np.ascontiguousarray(a[sl]))
+    sub.bc = {"W": "wall", "E": "wall", "S": "wall", "N": "wall"}
+    sub.inflow = {}
+    t0 = time.perf_counter()
+    r = oracle.run(sub, nsteps=steps, t_end=float("inf"))
+    secs = time.perf_counter() - t0
+    return crop * crop * r["steps"] / secs, r["counters"], secs, r["steps"]
+
+
+def f_alg_from_counters(cnt, cfg, steps, cells):
+    """Algorithmic fp64 ops per cell-update from the oracle's branch counters."""
+    ops = cnt.cell_stage * OPS_CELL_STAGE
+    ops += cnt.face_dry * OPS_FACE["dry"] + cnt.face_left * OPS_FACE["left"]
+    ops += cnt.face_right * OPS_FACE["right"] + cnt.face_mid * OPS_FACE["mid"]
+    if cfg.ga is not None:
+        ops += cnt.cell_stage * OPS_GA
+    if cfg.fric_law != "none":
+        ops += cnt.cell_wet_fric * OPS_FRIC_WET[cfg.fric_law]
+        if cfg.fric_field is not None:
+            ops += cnt.cell_wet_fric * OPS_FIELD
+    ops += steps * cells * OPS_STEP
+    return ops / (steps * cells)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--nx", type=int, default=None)
+    ap.add_argument("--ny", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-crop", type=int, default=1024)
+    ap.add_argument("--cpu-steps", type=int, default=12)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = dist_env()
+    from workloads import make
+
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_1307_4839_b200 import Solver, params_from_config
+
+    cfg = make(args.config, nx=args.nx, ny=args.ny)
+    cells = cfg.nx * cfg.ny
+    stream = torch.cuda.Stream()
+    solver = Solver(params_from_config(cfg), cfg.z, cfg.fric_field, stream=stream)
+    v0 = cfg.vinf if cfg.ga is not None else None
+    solver.set_state(cfg.h, cfg.hu, cfg.hv, v0, 0.0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident throughput (value) ----
+    solver.step(args.warmup)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record(stream)
+        solver.step(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    value = world * cells * args.steps / (ms / 1e3)
+    d = solver.diag()
+
+    # ---- per-kernel device time (eager launches with events around each kernel) ----
+    kp = min(args.steps, 20)
+    ms_k = solver.step_profiled(kp)
+    ms_pred, ms_corr = ms_k[0] / kp, ms_k[1] / kp
+
+    # ---- end to end through the public API: pinned host state in, K steps, state out ----
+    pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(cfg, k))).pin_memory() for k in ("h", "hu", "hv")}
+    if cfg.ga is not None:
+        pin["v"] = torch.from_numpy(np.ascontiguousarray(cfg.vinf)).pin_memory()
+    outp = {k: torch.empty_like(v).pin_memory() for k, v in pin.items()}
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    solver.set_state(pin["h"], pin["hu"], pin["hv"], pin.get("v"), 0.0)
+    solver.step(args.steps)
+    solver.get_state(outp["h"], outp["hu"], outp["hv"], outp.get("v"))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    nfield = len(pin)
+    io_bytes = nfield * cells * 8
+    e2e = {"value": world * cells * args.steps / (ms_e2e / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": io_bytes / args.steps, "d2h_bytes_per_step": io_bytes / args.steps,
+           "ms_total": ms_e2e, "note": "set_state from pinned host + K steps + get_state to pinned host"}
+
+    if rank != 0:
+        solver.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks, src = load_peaks()
+    ga, field = cfg.ga is not None, cfg.fric_field is not None
+    bp, bc = bytes_per_cell_update(ga, field)
+    dom = "corrector" if ms_corr >= ms_pred else "predictor"
+    dom_ms = max(ms_corr, ms_pred)
+    dom_bytes = (bc if dom == "corrector" else bp) * cells
+    hbm_achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg4 recipe, SURVEY.md §8d)",
+        "config": {"workload": args.config, "nx": cfg.nx, "ny": cfg.ny, "cells": cells,
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs (>=4.6 GB of fields) larger than L2; no flush"},
+        "e2e": e2e,
+        "gpu_launches": args.steps * Solver.launches_per_step(),
+        "kernels_ms": {"predictor": ms_pred, "corrector": ms_corr},
+        "hbm": {"dominant_kernel": dom, "achieved_gbs": hbm_achieved, "peak_gbs": peaks["hbm_gbs"],
+                "frac": hbm_achieved / peaks["hbm_gbs"], "bytes_per_cell_update": bp + bc, "peak_source": src},
+        "clocks": clk.summary(),
+        "diag": {"t": d["t"], "step": d["step"], "volume": d["volume"], "clamps": d["clamps"], "flags": d["flags"]},
+    }
+
+    fmax_mhz = peaks.get("sm_max_mhz", 1965.0)
+    peak_gops = 148 * 64 * fmax_mhz * 1e6 / 1e9        # fp64 lanes x SMs x clock
+    f_alg = None
+    if not args.no_cpu_baseline:
+        rate, cnt, secs, nst = cpu_sample(cfg, min(args.cpu_crop, cfg.nx, cfg.ny), args.cpu_steps)
+        crop = min(args.cpu_crop, cfg.nx, cfg.ny)
+        f_alg = f_alg_from_counters(cnt, cfg, nst, crop * crop)
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                               "sample": f"{crop}x{crop} centre crop of {args.config}, {nst} Heun steps, "
+                                         f"walls, {secs:.1f} s single-threaded"}
+    if f_alg is not None:
+        # dominant kernel's algorithmic fp64 ops: about half the per-step ops each (per-stage work)
+        frac_dom = (OPS_STEP / 2 + (f_alg - OPS_STEP) / 2) / f_alg if dom == "predictor" else \
+            ((f_alg - OPS_STEP) / 2 + OPS_STEP) / f_alg
+        ach = f_alg * frac_dom * cells / (dom_ms / 1e3) / 1e9
+        out["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak_gops, "unit": "Gop/s (fp64)",
+                           "frac": ach / peak_gops, "traffic": None, "kernel": dom,
+                           "f_alg_per_cell_update": f_alg,
+                           "peak_note": f"148 SMs x 64 fp64 lanes x {fmax_mhz:.0f} MHz (sm_max, {src})"}
+    print(json.dumps(out), flush=True)
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the oracle (plain single-threaded C), as it stands, on the host cores; each step
+    is one Heun step on a bounded crop of the workload."""
+    if rank != 0:
+        return
+    import oracle
+    from workloads import make
+    cfg = make(args.config, nx=args.nx, ny=args.ny)
+    crop = min(512, cfg.nx, cfg.ny)
+    # warm-up then timed steps, each a single Heun step of the crop
+    rate_w, _, _, _ = cpu_sample(cfg, crop, args.warmup)
+    rate, cnt, secs, nst = cpu_sample(cfg, crop, args.steps)
+    out = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": secs * 1e3 / max(nst, 1), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config, "nx": cfg.nx, "ny": cfg.ny, "sample": f"{crop}x{crop} crop"},
+           "impl": "reference",
+           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"{crop}x{crop} centre crop of {args.config}, {nst} Heun steps"},
+           "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

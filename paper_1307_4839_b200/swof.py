@@ -1,0 +1,239 @@
+"""Thin ctypes binding of libswof.so (include/swof.h): argument marshalling only.
+
+Every step of the time loop runs in the CUDA kernels of csrc/; there is no CPU path.  PyTorch is used
+only for device memory (the workspace) and the CUDA stream.  Importing this module without the
+built library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "libswof.so"
+
+SWOF_OK, SWOF_EINVAL, SWOF_ENUMERIC, SWOF_ECUDA, SWOF_ENOMEM, SWOF_ESTATE = range(6)
+FRIC = {"none": 0, "manning": 1, "strickler": 2, "darcy_weisbach": 3, "chezy": 4}
+BC = {"wall": 0, "free": 1, "periodic": 2, "inflow": 3}
+SIDES = ("W", "E", "S", "N")
+MAXT = 16
+FLAG_NONFINITE, FLAG_BIGCLAMP, FLAG_BADINPUT = 1, 2, 4
+EXPORTS = ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run", "swof_get_state",
+           "swof_get_dt_history", "swof_get_diag", "swof_predictor", "swof_step_profiled",
+           "swof_launches_per_step", "swof_destroy", "swof_last_error", "swof_strerror")
+
+
+class SwofParams(C.Structure):
+    """Mirror of `swof_params` (include/swof.h)."""
+    _fields_ = [
+        ("nx", C.c_int32), ("ny", C.c_int32), ("dx", C.c_double), ("dy", C.c_double),
+        ("g", C.c_double), ("cfl", C.c_double), ("dt_max", C.c_double), ("h_eps", C.c_double),
+        ("fric_law", C.c_int32), ("fric_coef", C.c_double),
+        ("ga_enabled", C.c_int32), ("ga_Ks", C.c_double), ("ga_hf", C.c_double), ("ga_A", C.c_double),
+        ("ga_dtheta", C.c_double), ("ga_vinf0", C.c_double),
+        ("n_rain", C.c_int32), ("rain_t", C.c_double * MAXT), ("rain_rate", C.c_double * MAXT),
+        ("bc", C.c_int32 * 4), ("inflow_k0", C.c_int32 * 4), ("inflow_k1", C.c_int32 * 4),
+        ("n_hydro", C.c_int32 * 4), ("hydro_t", (C.c_double * MAXT) * 4), ("hydro_q", (C.c_double * MAXT) * 4),
+        ("dt_hist_cap", C.c_int64), ("graph_steps", C.c_int32),
+    ]
+
+
+class SwofDiag(C.Structure):
+    """Mirror of `swof_diag` (include/swof.h)."""
+    _fields_ = [("t", C.c_double), ("step", C.c_int64), ("dt_next", C.c_double), ("volume", C.c_double),
+                ("vinf_volume", C.c_double), ("h_min", C.c_double), ("h_max", C.c_double),
+                ("wet_cells", C.c_int64), ("clamps", C.c_int64), ("clamped_mass", C.c_double),
+                ("clamp_max", C.c_double), ("flags", C.c_uint32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class SwofError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"swof error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libswof.so; raises if it is missing (no fallback of any kind)."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise ImportError(f"{_LIB_PATH} not built: run `python -m paper_1307_4839_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(str(_LIB_PATH))
+        vp, dp, i64p = C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)
+        PP = C.POINTER(SwofParams)
+        L.swof_workspace_size.argtypes = [PP, C.POINTER(C.c_size_t)]
+        L.swof_create.argtypes = [PP, dp, dp, vp, C.c_size_t, vp, C.POINTER(C.c_void_p)]
+        L.swof_set_state.argtypes = [vp, dp, dp, dp, dp, C.c_double]
+        L.swof_step.argtypes = [vp, C.c_int64]
+        L.swof_run.argtypes = [vp, C.c_double, C.c_int64, i64p]
+        L.swof_get_state.argtypes = [vp, dp, dp, dp, dp, C.POINTER(C.c_double), i64p]
+        L.swof_get_dt_history.argtypes = [vp, dp, C.c_int64, i64p]
+        L.swof_get_diag.argtypes = [vp, C.POINTER(SwofDiag)]
+        L.swof_predictor.argtypes = [vp, dp, dp, dp, dp]
+        L.swof_step_profiled.argtypes = [vp, C.c_int64, C.POINTER(C.c_double)]
+        L.swof_launches_per_step.argtypes = []
+        L.swof_destroy.argtypes = [vp]
+        L.swof_destroy.restype = None
+        L.swof_last_error.argtypes = [vp]
+        L.swof_last_error.restype = C.c_char_p
+        L.swof_strerror.argtypes = [C.c_int]
+        L.swof_strerror.restype = C.c_char_p
+        for name in ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run",
+                     "swof_get_state", "swof_get_dt_history", "swof_get_diag", "swof_predictor",
+                     "swof_step_profiled", "swof_launches_per_step"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def params_from_config(cfg, graph_steps: int = 0, dt_hist_cap: int = 0) -> SwofParams:
+    """Problem statement (a workloads.SwofConfig or any object with the same attributes) -> swof_params."""
+    p = SwofParams()
+    p.nx, p.ny, p.dx, p.dy = cfg.nx, cfg.ny, cfg.dx, cfg.dy
+    p.g, p.cfl, p.dt_max, p.h_eps = cfg.g, cfg.cfl, cfg.dt_max, cfg.h_eps
+    p.fric_law, p.fric_coef = FRIC[cfg.fric_law], cfg.fric_coef
+    if cfg.ga is not None:
+        p.ga_enabled = 1
+        p.ga_Ks, p.ga_hf, p.ga_A, p.ga_dtheta, p.ga_vinf0 = cfg.ga.Ks, cfg.ga.hf, cfg.ga.A, cfg.ga.dtheta, cfg.ga.vinf0
+    p.n_rain = len(cfg.rain_rate)
+    for k, (t, r) in enumerate(zip(cfg.rain_t, cfg.rain_rate)):
+        p.rain_t[k], p.rain_rate[k] = t, r
+    for s, side in enumerate(SIDES):
+        p.bc[s] = BC[cfg.bc[side]]
+        fl = cfg.inflow.get(side) if cfg.inflow else None
+        if fl is not None:
+            p.inflow_k0[s], p.inflow_k1[s] = fl.k0, fl.k1
+            p.n_hydro[s] = len(fl.hydro_t)
+            for k, (t, q) in enumerate(zip(fl.hydro_t, fl.hydro_q)):
+                p.hydro_t[s][k], p.hydro_q[s][k] = t, q
+    p.dt_hist_cap = dt_hist_cap
+    p.graph_steps = graph_steps
+    return p
+
+
+def _ptr(a, shape):
+    """Host numpy array or torch tensor (host or CUDA) -> raw pointer; fp64, C-contiguous, (ny, nx)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):                       # torch.Tensor
+        import torch
+        assert a.dtype == torch.float64 and a.is_contiguous() and tuple(a.shape) == shape, (a.dtype, a.shape)
+        return C.c_void_p(a.data_ptr())
+    assert isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.shape == shape, \
+        (type(a), getattr(a, "dtype", None), getattr(a, "shape", None))
+    return C.c_void_p(a.ctypes.data)
+
+
+class Solver:
+    """One swof_ctx: a grid advanced on one GPU.  `stream`: a torch.cuda.Stream (default: current)."""
+
+    def __init__(self, params: SwofParams, z, fric_field=None, stream=None, use_torch_workspace: bool = True,
+                 device=None):
+        import torch
+        self._L = lib()
+        self.params = params
+        self.shape = (params.ny, params.nx)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(self.device):
+            self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+            nbytes = C.c_size_t()
+            self._check(self._L.swof_workspace_size(C.byref(params), C.byref(nbytes)), None)
+            self.workspace_bytes = nbytes.value
+            self._ws = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device) if use_torch_workspace else None
+            ctx = C.c_void_p()
+            rc = self._L.swof_create(C.byref(params), _ptr(z, self.shape), _ptr(fric_field, self.shape),
+                                     C.c_void_p(self._ws.data_ptr()) if self._ws is not None else None,
+                                     nbytes.value, C.c_void_p(self.stream.cuda_stream), C.byref(ctx))
+            if rc != SWOF_OK:
+                raise SwofError(rc, self._L.swof_strerror(rc).decode())
+            self._ctx = ctx
+
+    # -- helpers
+    def _check(self, rc, ctx=None):
+        if rc != SWOF_OK:
+            msg = self._L.swof_last_error(ctx if ctx is not None else getattr(self, "_ctx", None)).decode() \
+                if (ctx is not None or getattr(self, "_ctx", None)) else self._L.swof_strerror(rc).decode()
+            raise SwofError(rc, msg)
+        return rc
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._L.swof_destroy(self._ctx)
+            self._ctx = None
+        self._ws = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- API (names follow include/swof.h)
+    def set_state(self, h, hu, hv, v_inf=None, t0: float = 0.0):
+        self._check(self._L.swof_set_state(self._ctx, _ptr(h, self.shape), _ptr(hu, self.shape), _ptr(hv, self.shape),
+                                           _ptr(v_inf, self.shape), float(t0)))
+
+    def step(self, nsteps: int):
+        self._check(self._L.swof_step(self._ctx, int(nsteps)))
+
+    def run(self, t_end: float, max_steps: int = 1 << 62) -> int:
+        n = C.c_int64()
+        self._check(self._L.swof_run(self._ctx, float(t_end), int(max_steps), C.byref(n)))
+        return n.value
+
+    def get_state(self, h=None, hu=None, hv=None, v_inf=None):
+        """Copy the state into the given arrays (numpy or torch, host or device); allocates numpy if None."""
+        out = {}
+        for k, a in (("h", h), ("hu", hu), ("hv", hv), ("v", v_inf)):
+            if a is None and (k != "v" or self.params.ga_enabled):
+                a = np.empty(self.shape)
+            out[k] = a
+        t, s = C.c_double(), C.c_int64()
+        self._check(self._L.swof_get_state(self._ctx, _ptr(out["h"], self.shape), _ptr(out["hu"], self.shape),
+                                           _ptr(out["hv"], self.shape), _ptr(out["v"], self.shape),
+                                           C.byref(t), C.byref(s)))
+        out["t"], out["step"] = t.value, s.value
+        return out
+
+    def predictor(self):
+        out = {k: np.empty(self.shape) for k in ("h", "hu", "hv")}
+        out["v"] = np.empty(self.shape) if self.params.ga_enabled else None
+        self._check(self._L.swof_predictor(self._ctx, _ptr(out["h"], self.shape), _ptr(out["hu"], self.shape),
+                                           _ptr(out["hv"], self.shape), _ptr(out["v"], self.shape)))
+        return out
+
+    def dt_history(self, cap: int = 1 << 22):
+        d = self.diag()
+        cap = min(cap, d["step"])
+        buf = np.empty(max(cap, 1))
+        n = C.c_int64()
+        self._check(self._L.swof_get_dt_history(self._ctx, C.c_void_p(buf.ctypes.data), cap, C.byref(n)))
+        return buf[: n.value]
+
+    def diag(self):
+        d = SwofDiag()
+        self._check(self._L.swof_get_diag(self._ctx, C.byref(d)))
+        return d.as_dict()
+
+    def step_profiled(self, nsteps: int):
+        ms = (C.c_double * 2)()
+        self._check(self._L.swof_step_profiled(self._ctx, int(nsteps), ms))
+        return ms[0], ms[1]
+
+    @staticmethod
+    def launches_per_step() -> int:
+        return lib().swof_launches_per_step()
