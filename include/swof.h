@@ -34,7 +34,7 @@ extern "C" {
 
 #define SWOF_OK 0
 #define SWOF_EINVAL 1    /* bad parameter / argument / initial state (h < 0 or non-finite)      */
-#define SWOF_ENUMERIC 2  /* NaN/Inf reached the CFL maximum, or one clamp of h exceeded 1e-10 m */
+#define SWOF_ENUMERIC 2  /* NaN/Inf reached the CFL maximum, or one clamp of h exceeded clamp_fail */
 #define SWOF_ECUDA 3     /* CUDA runtime failure                                                */
 #define SWOF_ENOMEM 4    /* device or pinned-host allocation failed / workspace too small       */
 #define SWOF_ESTATE 5    /* call order: swof_step/run/get_state before swof_set_state            */
@@ -60,7 +60,7 @@ extern "C" {
 
 /* diagnostic flags */
 #define SWOF_FLAG_NONFINITE 1u  /* NaN/Inf in the CFL maximum -> stepping halted                 */
-#define SWOF_FLAG_BIGCLAMP 2u   /* a single negative-height clamp larger than 1e-10 m            */
+#define SWOF_FLAG_BIGCLAMP 2u   /* a single negative-height clamp larger than params.clamp_fail  */
 #define SWOF_FLAG_BADINPUT 4u   /* set_state saw h < 0 or a non-finite value                     */
 
 typedef struct swof_params {
@@ -89,6 +89,8 @@ typedef struct swof_params {
     double hydro_q[4][SWOF_MAX_TABLE];  /* Q [m^3/s] over the segment; piecewise linear, clamped  */
     int64_t dt_hist_cap;     /* dt history capacity (0 -> 1<<20 steps)                             */
     int32_t graph_steps;     /* Heun steps per captured CUDA graph (0 -> 16; rounded up to even)  */
+    double clamp_fail;       /* a single negative-height clamp above this [m] raises SWOF_FLAG_BIGCLAMP
+                                and SWOF_ENUMERIC (0 -> 1e-6 m; DESIGN.md §3 Q17)                  */
 } swof_params;
 
 typedef struct swof_diag {
@@ -103,6 +105,8 @@ typedef struct swof_diag {
     double clamped_mass;     /* sum of the clamped -h' [m] (per cell, not times the area)         */
     double clamp_max;        /* largest single clamp [m]                                          */
     uint32_t flags;          /* SWOF_FLAG_* (sticky until set_state)                              */
+    int64_t big_clamp_cell;  /* row-major index j*nx+i of the largest clamp so far, -1 if none     */
+    int64_t big_clamp_step;  /* step in which that clamp happened, -1 if none                     */
 } swof_diag;
 
 typedef struct swof_ctx swof_ctx;

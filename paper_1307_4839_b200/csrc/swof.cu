@@ -103,6 +103,7 @@ const char* validate(const swof_params* p) {
         return "periodic boundaries must be paired (W/E, S/N)";
     if (p->dt_hist_cap < 0) return "dt_hist_cap must be >= 0";
     if (p->graph_steps < 0) return "graph_steps must be >= 0";
+    if (!(p->clamp_fail >= 0)) return "clamp_fail must be >= 0";
     return nullptr;
 }
 
@@ -172,7 +173,7 @@ int read_state(swof_ctx* c) {
 int flags_rc(swof_ctx* c) {
     if (c->h_st->flags & (FLAG_NONFINITE | FLAG_BIGCLAMP)) {
         return fail(c, SWOF_ENUMERIC, (c->h_st->flags & FLAG_NONFINITE) ? "non-finite value reached the CFL maximum"
-                                                                         : "a negative-height clamp exceeded 1e-10 m");
+                                                                         : "a negative-height clamp exceeded clamp_fail");
     }
     return SWOF_OK;
 }
@@ -267,6 +268,7 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     k.fric_law = p->fric_law; k.has_fric_field = has_ff; k.ga = p->ga_enabled != 0;
     k.dx = p->dx; k.dy = p->dy; k.g = p->g; k.cfl = p->cfl; k.dt_max = p->dt_max; k.h_eps = p->h_eps;
     k.fric_coef = p->fric_coef;
+    k.clamp_fail = p->clamp_fail > 0 ? p->clamp_fail : 1e-6;
     k.Ks = p->ga_Ks; k.hf = p->ga_hf; k.A = p->ga_A; k.dtheta = p->ga_dtheta;
     k.n_rain = p->n_rain;
     for (int i = 0; i < p->n_rain; ++i) { k.rain_t[i] = p->rain_t[i]; k.rain_rate[i] = p->rain_rate[i]; }
@@ -316,6 +318,8 @@ int swof_set_state(swof_ctx* c, const double* h, const double* hu, const double*
     s.t[0] = t0;
     s.t_end = INFINITY;
     s.step_limit = INT64_MAX;
+    s.big_clamp_cell = -1;
+    s.big_clamp_step = -1;
     *c->h_st = s;
     CK(cudaMemcpyAsync(c->kb.st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
     init_cfl_kernel<<<1184, 256, 0, c->stream>>>(c->kp, c->kb);
@@ -437,6 +441,8 @@ int swof_get_diag(swof_ctx* c, swof_diag* d) {
     d->clamped_mass = s.clamped_mass;
     std::memcpy(&d->clamp_max, &s.clamp_max_bits, 8);
     d->flags = s.flags;
+    d->big_clamp_cell = s.big_clamp_cell;
+    d->big_clamp_step = s.big_clamp_step;
     return SWOF_OK;
 }
 

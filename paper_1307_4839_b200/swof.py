@@ -35,7 +35,7 @@ class SwofParams(C.Structure):
         ("n_rain", C.c_int32), ("rain_t", C.c_double * MAXT), ("rain_rate", C.c_double * MAXT),
         ("bc", C.c_int32 * 4), ("inflow_k0", C.c_int32 * 4), ("inflow_k1", C.c_int32 * 4),
         ("n_hydro", C.c_int32 * 4), ("hydro_t", (C.c_double * MAXT) * 4), ("hydro_q", (C.c_double * MAXT) * 4),
-        ("dt_hist_cap", C.c_int64), ("graph_steps", C.c_int32),
+        ("dt_hist_cap", C.c_int64), ("graph_steps", C.c_int32), ("clamp_fail", C.c_double),
     ]
 
 
@@ -44,7 +44,8 @@ class SwofDiag(C.Structure):
     _fields_ = [("t", C.c_double), ("step", C.c_int64), ("dt_next", C.c_double), ("volume", C.c_double),
                 ("vinf_volume", C.c_double), ("h_min", C.c_double), ("h_max", C.c_double),
                 ("wet_cells", C.c_int64), ("clamps", C.c_int64), ("clamped_mass", C.c_double),
-                ("clamp_max", C.c_double), ("flags", C.c_uint32)]
+                ("clamp_max", C.c_double), ("flags", C.c_uint32),
+                ("big_clamp_cell", C.c_int64), ("big_clamp_step", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
