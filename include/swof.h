@@ -160,6 +160,11 @@ int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms);
 /* Number of kernel launches one Heun step issues (2). */
 int swof_launches_per_step(void);
 
+/* Self-test of the kernels' slow-path-free IEEE reciprocal, division and square root against CUDA's
+ * library operators on n random operands (exponents in [-60, 60], sqrt in [-80, 40]) on the current
+ * device; mismatches[0..2] receive the bitwise mismatch counts (rcp, div, sqrt), all 0 when exact. */
+int swof_selftest_math(int64_t n, uint64_t seed, int64_t* mismatches);
+
 void swof_destroy(swof_ctx* c);
 const char* swof_last_error(const swof_ctx* c);
 const char* swof_strerror(int code);

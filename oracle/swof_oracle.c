@@ -31,7 +31,8 @@ double or_minmod(double a, double b) {
 }
 
 /* Canonical inverse cube root x^(-1/3) for finite x > 0: exponent split
- * x = m' 2^(3q) with m' in [0.5, 4), chord initial guess on the octave of m', then 5 Newton steps
+ * x = m' 2^(3q) with m' in [0.5, 4), chord initial guess on the octave of m' (<= 2.7 % error), then
+ * 4 Newton steps (error 2.7e-2 -> 1.5e-3 -> 4.3e-6 -> 3.7e-11 -> 2.7e-21)
  * y <- y + y (1 - m' y^3) / 3.  Used for h^(4/3) in Manning/Strickler friction and the
  * critical depth of the inflow ghost (Q18).  Pinned against libm cbrt in tests/test_oracle_unit.py. */
 double or_icbrt(double x) {
@@ -46,7 +47,7 @@ double or_icbrt(double x) {
     else { lo = 2.0; yl = 0.7937005259840998; yh = 0.6299605249474366; }
     double y = yl + (yh - yl) * ((mp - lo) / lo);
     const double third = 1.0 / 3.0;
-    for (int it = 0; it < 5; ++it) {
+    for (int it = 0; it < 4; ++it) {
         double y3 = (y * y) * y;
         double t = 1.0 - mp * y3;
         y = y + (y * t) * third;
@@ -203,9 +204,9 @@ void or_friction(double gcf, int law, double h_eps, double dt, double hs, double
     } else {
         w = k / hst;
     }
-    double d = 1.0 + w;
-    *hu_out = hup / d;
-    *hv_out = hvp / d;
+    double rd = 1.0 / (1.0 + w); /* q* / (1 + ...) evaluated as q* (1 / (1 + ...)) */
+    *hu_out = hup * rd;
+    *hv_out = hvp * rd;
 }
 
 /* ------------------------------------------------------------------------------------------ */

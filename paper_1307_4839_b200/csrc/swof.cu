@@ -204,6 +204,20 @@ extern "C" {
 
 int swof_launches_per_step(void) { return 2; }
 
+int swof_selftest_math(int64_t n, uint64_t seed, int64_t* mismatches) {
+    if (n < 0 || !mismatches) return SWOF_EINVAL;
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, 3 * sizeof(unsigned long long)) != cudaSuccess) return SWOF_ENOMEM;
+    cudaMemset(d, 0, 3 * sizeof(unsigned long long));
+    selftest_math_kernel<<<1184, 256>>>((long long)n, (unsigned long long)seed, d);
+    unsigned long long h[3] = {0, 0, 0};
+    cudaError_t e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return SWOF_ECUDA;
+    for (int i = 0; i < 3; ++i) mismatches[i] = (int64_t)h[i];
+    return SWOF_OK;
+}
+
 const char* swof_strerror(int code) {
     switch (code) {
         case SWOF_OK: return "ok";

@@ -21,7 +21,7 @@ MAXT = 16
 FLAG_NONFINITE, FLAG_BIGCLAMP, FLAG_BADINPUT = 1, 2, 4
 EXPORTS = ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run", "swof_get_state",
            "swof_get_dt_history", "swof_get_diag", "swof_predictor", "swof_step_profiled",
-           "swof_launches_per_step", "swof_destroy", "swof_last_error", "swof_strerror")
+           "swof_launches_per_step", "swof_selftest_math", "swof_destroy", "swof_last_error", "swof_strerror")
 
 
 class SwofParams(C.Structure):
@@ -81,6 +81,7 @@ def lib():
         L.swof_predictor.argtypes = [vp, dp, dp, dp, dp]
         L.swof_step_profiled.argtypes = [vp, C.c_int64, C.POINTER(C.c_double)]
         L.swof_launches_per_step.argtypes = []
+        L.swof_selftest_math.argtypes = [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]
         L.swof_destroy.argtypes = [vp]
         L.swof_destroy.restype = None
         L.swof_last_error.argtypes = [vp]
@@ -89,7 +90,7 @@ def lib():
         L.swof_strerror.restype = C.c_char_p
         for name in ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run",
                      "swof_get_state", "swof_get_dt_history", "swof_get_diag", "swof_predictor",
-                     "swof_step_profiled", "swof_launches_per_step"):
+                     "swof_step_profiled", "swof_launches_per_step", "swof_selftest_math"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -238,3 +239,12 @@ class Solver:
     @staticmethod
     def launches_per_step() -> int:
         return lib().swof_launches_per_step()
+
+
+def selftest_math(n: int = 1 << 24, seed: int = 1307):
+    """Bitwise mismatches (rcp, div, sqrt) of the kernels' IEEE operations vs CUDA's library ones."""
+    out = (C.c_int64 * 3)()
+    rc = lib().swof_selftest_math(int(n), int(seed), out)
+    if rc != SWOF_OK:
+        raise SwofError(rc, "selftest_math failed")
+    return tuple(out)
