@@ -106,6 +106,23 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def reduce_max(x: float, world: int, device=None) -> float:
+    """Max of a per-rank scalar over all ranks (identity on one rank)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_rate(world: int, cells: int, steps: int, max_ms: float) -> float:
+    """Whole-job cell-updates/s: every rank advanced its own replica by `steps` steps; the job took the
+    slowest rank's time."""
+    return world * cells * steps / (max_ms / 1e3)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -189,11 +206,7 @@ def main():
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(x, world, "cuda")
 
     # ---- device-resident throughput (value) ----
     solver.step(args.warmup)
@@ -207,7 +220,7 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
-    value = world * cells * args.steps / (ms / 1e3)
+    value = aggregate_rate(world, cells, args.steps, ms)
     d = solver.diag()
 
     # ---- per-kernel device time (eager launches with events around each kernel) ----
@@ -233,7 +246,7 @@ def main():
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
     nfield = len(pin)
     io_bytes = nfield * cells * 8
-    e2e = {"value": world * cells * args.steps / (ms_e2e / 1e3), "unit": UNIT,
+    e2e = {"value": aggregate_rate(world, cells, args.steps, ms_e2e), "unit": UNIT,
            "h2d_bytes_per_step": io_bytes / args.steps, "d2h_bytes_per_step": io_bytes / args.steps,
            "ms_total": ms_e2e, "note": "set_state from pinned host + K steps + get_state to pinned host"}
 

@@ -19,3 +19,14 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file
 echo "ncu rc=$?" >> gpurun_out/ncu_list.log ;;
 esac
 done
+# full-size variants (the bench's own launch configuration)
+for what in "$@"; do
+case $what in
+ncu8k)
+CMD="python bench.py --steps 4 --warmup 3 --no-cpu-baseline"
+$CMD > gpurun_out/plain8k.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches8k.csv $CMD > gpurun_out/ncu_list8k.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 6 -c 2 -o gpurun_out/prof8k $CMD > gpurun_out/ncu_full8k.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_full8k.log ;;
+esac
+done
