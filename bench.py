@@ -295,8 +295,19 @@ def main():
         frac_dom = (OPS_STEP / 2 + (f_alg - OPS_STEP) / 2) / f_alg if dom == "predictor" else \
             ((f_alg - OPS_STEP) / 2 + OPS_STEP) / f_alg
         ach = f_alg * frac_dom * cells / (dom_ms / 1e3) / 1e9
+        traffic, tsrc = None, None
+        try:   # DRAM read+write per launch of the same kernel from the committed ncu --set full capture
+            with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
+                prof = json.load(f)
+            for kname, k in prof["kernels"].items():
+                if ("<1>" in kname) == (dom == "corrector"):
+                    traffic = k["dram_bytes_per_cell"] * cells
+                    tsrc = f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"
+        except Exception:
+            pass
         out["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak_gops, "unit": "Gop/s (fp64)",
-                           "frac": ach / peak_gops, "traffic": None, "kernel": dom,
+                           "frac": ach / peak_gops, "traffic": traffic, "traffic_unit": "bytes/launch",
+                           "traffic_source": tsrc, "algorithmic_bytes": dom_bytes, "kernel": dom,
                            "f_alg_per_cell_update": f_alg,
                            "peak_note": f"148 SMs x 64 fp64 lanes x {fmax_mhz:.0f} MHz (sm_max, {src})"}
     print(json.dumps(out), flush=True)
