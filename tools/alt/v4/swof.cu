@@ -1,0 +1,524 @@
+// swof.cu -- C ABI (include/swof.h) of the B200-native FullSWOF_2D time step.
+//
+// Host side: parameter validation, workspace layout (padded SoA fp64 fields, 256-B aligned rows),
+// device scalar state double-buffered by step parity, the step loop captured as a CUDA graph of
+// `graph_steps` Heun steps (2 launches each), and fixed-order diagnostics.  No host round trip per
+// step: every CTA derives dt_n from the CFL maxima the previous corrector left in device memory.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "swof.h"
+#include "swof_kernels.cuh"
+
+using namespace swof;
+
+struct swof_ctx {
+    swof_params p;
+    KParams kp;
+    KBufs kb;
+    void* ws = nullptr;
+    bool own_ws = false;
+    size_t ws_bytes = 0;
+    cudaStream_t stream = nullptr;
+    int par = 0;                       // parity of the next step to launch
+    bool have_state = false;
+    int graph_steps = 16;
+    cudaGraphExec_t graph = nullptr;   // graph_steps steps starting at parity 0
+    DevState* h_st = nullptr;          // pinned mirror of the device scalar state
+    double* d_part = nullptr;          // diag partials
+    int diag_blocks = 0;
+    dim3 grid;
+    std::string err;
+};
+
+namespace {
+
+constexpr int DIAG_BLOCKS = 1184;      // 8 x 148 SMs
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+    size_t pitch;                      // doubles per row
+    size_t field;                      // bytes per field
+    size_t off_A, off_B, off_z, off_VA, off_VB, off_fric, off_st, off_hist, off_part, total;
+};
+
+Layout make_layout(const swof_params* p, bool fric_field) {
+    Layout L{};
+    L.pitch = align_up((size_t)p->nx, 32);
+    L.field = align_up(L.pitch * sizeof(double) * (size_t)p->ny, 256);
+    size_t o = 0;
+    L.off_A = o; o += 3 * L.field;
+    L.off_B = o; o += 3 * L.field;
+    L.off_z = o; o += L.field;
+    L.off_VA = o; o += p->ga_enabled ? L.field : 0;
+    L.off_VB = o; o += p->ga_enabled ? L.field : 0;
+    L.off_fric = o; o += fric_field ? L.field : 0;
+    L.off_st = o; o += align_up(sizeof(DevState), 256);
+    int64_t cap = p->dt_hist_cap > 0 ? p->dt_hist_cap : (int64_t)1 << 20;
+    L.off_hist = o; o += align_up((size_t)cap * sizeof(double), 256);
+    L.off_part = o; o += align_up((size_t)DIAG_BLOCKS * 5 * sizeof(double), 256);
+    L.total = o;
+    return L;
+}
+
+const char* validate(const swof_params* p) {
+    if (!p) return "params is NULL";
+    if (p->nx < 1 || p->ny < 1) return "nx, ny must be >= 1";
+    if (!(p->dx > 0) || !(p->dy > 0) || !std::isfinite(p->dx) || !std::isfinite(p->dy)) return "dx, dy must be finite and > 0";
+    if (!(p->g > 0) || !std::isfinite(p->g)) return "g must be > 0";
+    if (!(p->cfl > 0) || p->cfl > 1) return "cfl must be in (0, 1]";
+    if (!(p->dt_max > 0) || !std::isfinite(p->dt_max)) return "dt_max must be finite and > 0";
+    if (!(p->h_eps >= 0) || !std::isfinite(p->h_eps)) return "h_eps must be finite and >= 0";
+    if (p->fric_law < SWOF_FRIC_NONE || p->fric_law > SWOF_FRIC_CHEZY) return "unknown fric_law";
+    if (p->ga_enabled) {
+        if (!(p->ga_Ks >= 0) || !(p->ga_dtheta > 0) || !std::isfinite(p->ga_hf) || !std::isfinite(p->ga_A) ||
+            !(p->ga_vinf0 >= 0))
+            return "Green-Ampt needs Ks >= 0, dtheta > 0, finite hf and A, vinf0 >= 0";
+    }
+    if (p->n_rain < 0 || p->n_rain > SWOF_MAX_TABLE) return "n_rain out of range";
+    for (int k = 0; k < p->n_rain; ++k) {
+        if (!(p->rain_rate[k] >= 0) || !std::isfinite(p->rain_rate[k])) return "rain rates must be finite and >= 0";
+        if (k > 0 && !(p->rain_t[k] > p->rain_t[k - 1])) return "rain_t must be ascending";
+    }
+    for (int s = 0; s < 4; ++s) {
+        if (p->bc[s] < SWOF_BC_WALL || p->bc[s] > SWOF_BC_INFLOW) return "unknown boundary type";
+        const int n = (s < 2) ? p->ny : p->nx;
+        if (p->bc[s] == SWOF_BC_INFLOW) {
+            if (p->inflow_k0[s] < 0 || p->inflow_k1[s] > n || p->inflow_k0[s] >= p->inflow_k1[s])
+                return "inflow segment out of range";
+            if (p->n_hydro[s] < 1 || p->n_hydro[s] > SWOF_MAX_TABLE) return "inflow needs 1..16 hydrograph points";
+            for (int k = 1; k < p->n_hydro[s]; ++k)
+                if (!(p->hydro_t[s][k] > p->hydro_t[s][k - 1])) return "hydro_t must be ascending";
+        }
+    }
+    if ((p->bc[0] == SWOF_BC_PERIODIC) != (p->bc[1] == SWOF_BC_PERIODIC) ||
+        (p->bc[2] == SWOF_BC_PERIODIC) != (p->bc[3] == SWOF_BC_PERIODIC))
+        return "periodic boundaries must be paired (W/E, S/N)";
+    if (p->dt_hist_cap < 0) return "dt_hist_cap must be >= 0";
+    if (p->graph_steps < 0) return "graph_steps must be >= 0";
+    if (!(p->clamp_fail >= 0)) return "clamp_fail must be >= 0";
+    return nullptr;
+}
+
+int fail(swof_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_fail(swof_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, SWOF_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                             \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
+    } while (0)
+
+void launch_step(swof_ctx* c, int par, cudaStream_t s) {
+    stage_kernel<false><<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
+    stage_kernel<true><<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
+}
+void launch_step(swof_ctx* c, int par) { launch_step(c, par, c->stream); }
+
+int build_graph(swof_ctx* c) {
+    if (c->graph) return SWOF_OK;
+    // capture on a private stream (the legacy default stream cannot be captured); the graph is
+    // then launched on the context's stream
+    cudaGraph_t g = nullptr;
+    cudaStream_t cs = nullptr;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        for (int k = 0; k < c->graph_steps; ++k) launch_step(c, k & 1, cs);
+        e = cudaStreamEndCapture(cs, &g);
+    }
+    cudaStreamDestroy(cs);
+    if (e != cudaSuccess) return cuda_fail(c, e, "graph capture");
+    e = cudaGraphInstantiate(&c->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) { c->graph = nullptr; return cuda_fail(c, e, "cudaGraphInstantiate"); }
+    return SWOF_OK;
+}
+
+// enqueue exactly n step launches (graph replays + eager remainder); keeps c->par in sync
+int enqueue_steps(swof_ctx* c, int64_t n) {
+    while (n > 0 && c->par != 0) { launch_step(c, c->par); c->par ^= 1; --n; }
+    if (n >= c->graph_steps) {
+        int rc = build_graph(c);
+        if (rc) return rc;
+        while (n >= c->graph_steps) {
+            CK(cudaGraphLaunch(c->graph, c->stream));
+            n -= c->graph_steps;
+        }
+    }
+    while (n > 0) { launch_step(c, c->par); c->par ^= 1; --n; }
+    CK(cudaGetLastError());
+    return SWOF_OK;
+}
+
+int read_state(swof_ctx* c) {
+    CK(cudaMemcpyAsync(c->h_st, c->kb.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SWOF_OK;
+}
+
+int flags_rc(swof_ctx* c) {
+    if (c->h_st->flags & (FLAG_NONFINITE | FLAG_BIGCLAMP)) {
+        return fail(c, SWOF_ENUMERIC, (c->h_st->flags & FLAG_NONFINITE) ? "non-finite value reached the CFL maximum"
+                                                                         : "a negative-height clamp exceeded clamp_fail");
+    }
+    return SWOF_OK;
+}
+
+int copy_field_in(swof_ctx* c, double* dst, const double* src) {
+    const size_t w = (size_t)c->p.nx * sizeof(double);
+    CK(cudaMemcpy2DAsync(dst, c->kp.pitch * sizeof(double), src, w, w, (size_t)c->p.ny, cudaMemcpyDefault, c->stream));
+    return SWOF_OK;
+}
+
+int copy_field_out(swof_ctx* c, double* dst, const double* src) {
+    const size_t w = (size_t)c->p.nx * sizeof(double);
+    CK(cudaMemcpy2DAsync(dst, w, src, c->kp.pitch * sizeof(double), w, (size_t)c->p.ny, cudaMemcpyDefault, c->stream));
+    return SWOF_OK;
+}
+
+__global__ void fill_kernel(double* a, int nx, int ny, int pitch, double v) {
+    const long long n = (long long)nx * ny;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(k / nx), i = (int)(k - (long long)j * nx);
+        a[(size_t)j * pitch + i] = v;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int swof_launches_per_step(void) { return 2; }
+
+int swof_selftest_math(int64_t n, uint64_t seed, int64_t* mismatches) {
+    if (n < 0 || !mismatches) return SWOF_EINVAL;
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, 3 * sizeof(unsigned long long)) != cudaSuccess) return SWOF_ENOMEM;
+    cudaMemset(d, 0, 3 * sizeof(unsigned long long));
+    selftest_math_kernel<<<1184, 256>>>((long long)n, (unsigned long long)seed, d);
+    unsigned long long h[3] = {0, 0, 0};
+    cudaError_t e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return SWOF_ECUDA;
+    for (int i = 0; i < 3; ++i) mismatches[i] = (int64_t)h[i];
+    return SWOF_OK;
+}
+
+const char* swof_strerror(int code) {
+    switch (code) {
+        case SWOF_OK: return "ok";
+        case SWOF_EINVAL: return "invalid argument";
+        case SWOF_ENUMERIC: return "numerical failure";
+        case SWOF_ECUDA: return "CUDA error";
+        case SWOF_ENOMEM: return "out of memory";
+        case SWOF_ESTATE: return "invalid call order";
+        default: return "unknown error";
+    }
+}
+
+const char* swof_last_error(const swof_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int swof_workspace_size(const swof_params* p, size_t* bytes) {
+    if (validate(p) || !bytes) return SWOF_EINVAL;
+    *bytes = make_layout(p, true).total;   // with room for a per-cell friction field
+    return SWOF_OK;
+}
+
+int swof_create(const swof_params* p, const double* z, const double* fric_field, void* d_workspace, size_t ws_bytes,
+                void* cuda_stream, swof_ctx** out) {
+    if (!out) return SWOF_EINVAL;
+    *out = nullptr;
+    if (validate(p) || !z) return SWOF_EINVAL;
+    if (p->fric_law == SWOF_FRIC_NONE && fric_field) return SWOF_EINVAL;
+    if (!fric_field && p->fric_law != SWOF_FRIC_NONE && !(p->fric_coef > 0)) return SWOF_EINVAL;
+    swof_ctx* c = new (std::nothrow) swof_ctx();
+    if (!c) return SWOF_ENOMEM;
+    c->p = *p;
+    c->stream = (cudaStream_t)cuda_stream;
+    c->graph_steps = p->graph_steps > 0 ? (p->graph_steps + 1) / 2 * 2 : 16;
+    const bool has_ff = fric_field != nullptr;
+    const Layout L = make_layout(p, has_ff);
+    if (d_workspace) {
+        if (ws_bytes < L.total || ((uintptr_t)d_workspace & 255)) { delete c; return SWOF_ENOMEM; }
+        c->ws = d_workspace;
+    } else {
+        if (cudaMalloc(&c->ws, L.total) != cudaSuccess) { delete c; return SWOF_ENOMEM; }
+        c->own_ws = true;
+    }
+    c->ws_bytes = L.total;
+    if (cudaMallocHost((void**)&c->h_st, sizeof(DevState)) != cudaSuccess) { swof_destroy(c); return SWOF_ENOMEM; }
+
+    char* base = (char*)c->ws;
+    KBufs& b = c->kb;
+    const size_t F = L.field;
+    b.Ah = (double*)(base + L.off_A); b.Ahu = (double*)(base + L.off_A + F); b.Ahv = (double*)(base + L.off_A + 2 * F);
+    b.Bh = (double*)(base + L.off_B); b.Bhu = (double*)(base + L.off_B + F); b.Bhv = (double*)(base + L.off_B + 2 * F);
+    b.z = (double*)(base + L.off_z);
+    b.VA = p->ga_enabled ? (double*)(base + L.off_VA) : nullptr;
+    b.VB = p->ga_enabled ? (double*)(base + L.off_VB) : nullptr;
+    b.fric = has_ff ? (double*)(base + L.off_fric) : nullptr;
+    b.st = (DevState*)(base + L.off_st);
+    b.dt_hist = (double*)(base + L.off_hist);
+    b.dt_cap = p->dt_hist_cap > 0 ? p->dt_hist_cap : (int64_t)1 << 20;
+    c->d_part = (double*)(base + L.off_part);
+
+    KParams& k = c->kp;
+    std::memset(&k, 0, sizeof(k));
+    k.nx = p->nx; k.ny = p->ny; k.pitch = (int)L.pitch;
+    k.fric_law = p->fric_law; k.has_fric_field = has_ff; k.ga = p->ga_enabled != 0;
+    k.dx = p->dx; k.dy = p->dy; k.g = p->g; k.cfl = p->cfl; k.dt_max = p->dt_max; k.h_eps = p->h_eps;
+    k.fric_coef = p->fric_coef;
+    k.clamp_fail = p->clamp_fail > 0 ? p->clamp_fail : 1e-6;
+    k.Ks = p->ga_Ks; k.hf = p->ga_hf; k.A = p->ga_A; k.dtheta = p->ga_dtheta;
+    k.n_rain = p->n_rain;
+    for (int i = 0; i < p->n_rain; ++i) { k.rain_t[i] = p->rain_t[i]; k.rain_rate[i] = p->rain_rate[i]; }
+    for (int s = 0; s < 4; ++s) {
+        k.bc[s] = p->bc[s];
+        k.k0[s] = p->inflow_k0[s]; k.k1[s] = p->inflow_k1[s];
+        k.n_hydro[s] = p->bc[s] == SWOF_BC_INFLOW ? p->n_hydro[s] : 0;
+        k.width[s] = (double)(p->inflow_k1[s] - p->inflow_k0[s]) * ((s < 2) ? p->dy : p->dx);
+        for (int i = 0; i < k.n_hydro[s]; ++i) { k.hydro_t[s][i] = p->hydro_t[s][i]; k.hydro_q[s][i] = p->hydro_q[s][i]; }
+    }
+    c->grid = dim3((unsigned)((p->nx + TX - 1) / TX), (unsigned)((p->ny + TY - 1) / TY));
+    c->diag_blocks = DIAG_BLOCKS;
+
+    cudaError_t e = cudaFuncSetAttribute(stage_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(stage_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->ws, 0, L.total, c->stream);
+    if (e != cudaSuccess) { int rc = cuda_fail(c, e, "swof_create"); fprintf(stderr, "swof: %s\n", c->err.c_str()); swof_destroy(c); return rc; }
+    int rc = copy_field_in(c, b.z, z);
+    if (!rc && has_ff) rc = copy_field_in(c, b.fric, fric_field);
+    if (!rc) { e = cudaStreamSynchronize(c->stream); if (e != cudaSuccess) rc = cuda_fail(c, e, "swof_create sync"); }
+    if (rc) { swof_destroy(c); return rc; }
+    if (has_ff) {
+        // per-cell coefficients must be > 0 (NonPositiveCoefficient)
+        std::vector<double> tmp((size_t)p->nx);
+        for (int j = 0; j < p->ny; ++j) {
+            if (cudaMemcpy(tmp.data(), b.fric + (size_t)j * L.pitch, tmp.size() * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) { swof_destroy(c); return SWOF_ECUDA; }
+            for (double v : tmp) if (!(v > 0) || !std::isfinite(v)) { swof_destroy(c); return SWOF_EINVAL; }
+        }
+    }
+    *out = c;
+    return SWOF_OK;
+}
+
+int swof_set_state(swof_ctx* c, const double* h, const double* hu, const double* hv, const double* v_inf, double t0) {
+    if (!c) return SWOF_EINVAL;
+    if (!h || !hu || !hv || !std::isfinite(t0)) return fail(c, SWOF_EINVAL, "set_state: h, hu, hv required, t0 finite");
+    int rc;
+    if ((rc = copy_field_in(c, c->kb.Ah, h)) || (rc = copy_field_in(c, c->kb.Ahu, hu)) || (rc = copy_field_in(c, c->kb.Ahv, hv)))
+        return rc;
+    if (c->kp.ga) {
+        if (v_inf) { if ((rc = copy_field_in(c, c->kb.VA, v_inf))) return rc; }
+        else fill_kernel<<<1184, 256, 0, c->stream>>>(c->kb.VA, c->p.nx, c->p.ny, c->kp.pitch, c->p.ga_vinf0);
+    }
+    DevState s;
+    std::memset(&s, 0, sizeof(s));
+    s.t[0] = t0;
+    s.t_end = INFINITY;
+    s.step_limit = INT64_MAX;
+    s.big_clamp_cell = -1;
+    s.big_clamp_step = -1;
+    *c->h_st = s;
+    CK(cudaMemcpyAsync(c->kb.st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+    init_cfl_kernel<<<1184, 256, 0, c->stream>>>(c->kp, c->kb);
+    CK(cudaGetLastError());
+    c->par = 0;
+    if ((rc = read_state(c))) return rc;
+    if (c->h_st->flags & FLAG_BADINPUT) {
+        c->have_state = false;
+        return fail(c, SWOF_EINVAL, "set_state: h < 0 or a non-finite value in the state");
+    }
+    c->have_state = true;
+    return SWOF_OK;
+}
+
+int swof_step(swof_ctx* c, int64_t nsteps) {
+    if (!c) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_step before swof_set_state");
+    if (nsteps < 0) return fail(c, SWOF_EINVAL, "nsteps < 0");
+    // no t_end clipping, no step limit
+    const double inf = INFINITY;
+    const long long lim = INT64_MAX;
+    CK(cudaMemcpyAsync(&c->kb.st->t_end, &inf, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(&c->kb.st->step_limit, &lim, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    int rc = enqueue_steps(c, nsteps);
+    if (rc) return rc;
+    if ((rc = read_state(c))) return rc;
+    return flags_rc(c);
+}
+
+int swof_run(swof_ctx* c, double t_end, int64_t max_steps, int64_t* steps_done) {
+    if (!c) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_run before swof_set_state");
+    if (max_steps < 0 || std::isnan(t_end)) return fail(c, SWOF_EINVAL, "swof_run: bad t_end / max_steps");
+    int rc;
+    if ((rc = read_state(c))) return rc;
+    const long long step0 = c->h_st->step[c->par];
+    const long long lim = step0 + max_steps;
+    CK(cudaMemcpyAsync(&c->kb.st->t_end, &t_end, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(&c->kb.st->step_limit, &lim, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    // replay until the device reports done (t >= t_end, step limit, or a halt); steps past the end
+    // are exact no-ops, so overshooting by a partial batch is harmless
+    int64_t batch = c->graph_steps;
+    for (;;) {
+        const long long cur = c->h_st->step[c->par];
+        const double tc = c->h_st->t[c->par];
+        if (!(tc < t_end) || cur >= lim || (c->h_st->flags & FLAG_NONFINITE)) break;
+        int64_t left = lim - cur;
+        int64_t n = left < batch ? left : batch;
+        if ((rc = enqueue_steps(c, n))) return rc;
+        if ((rc = read_state(c))) return rc;
+        if (batch < 64 * c->graph_steps) batch *= 2;
+    }
+    if (steps_done) *steps_done = c->h_st->step[c->par] - step0;
+    return flags_rc(c);
+}
+
+int swof_get_state(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf, double* t, int64_t* step) {
+    if (!c) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_get_state before swof_set_state");
+    int rc;
+    if (h && (rc = copy_field_out(c, h, c->kb.Ah))) return rc;
+    if (hu && (rc = copy_field_out(c, hu, c->kb.Ahu))) return rc;
+    if (hv && (rc = copy_field_out(c, hv, c->kb.Ahv))) return rc;
+    if (v_inf && c->kp.ga && (rc = copy_field_out(c, v_inf, c->kb.VA))) return rc;
+    if ((rc = read_state(c))) return rc;
+    if (t) *t = c->h_st->t[c->par];
+    if (step) *step = c->h_st->step[c->par];
+    return SWOF_OK;
+}
+
+int swof_get_dt_history(swof_ctx* c, double* dt, int64_t cap, int64_t* n) {
+    if (!c || (!dt && cap > 0) || cap < 0) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_get_dt_history before swof_set_state");
+    int rc;
+    if ((rc = read_state(c))) return rc;
+    long long steps = c->h_st->step[c->par];
+    long long m = steps < c->kb.dt_cap ? steps : c->kb.dt_cap;
+    if (m > cap) m = cap;
+    if (m > 0) {
+        CK(cudaMemcpyAsync(dt, c->kb.dt_hist, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    if (n) *n = m;
+    return SWOF_OK;
+}
+
+int swof_get_diag(swof_ctx* c, swof_diag* d) {
+    if (!c || !d) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_get_diag before swof_set_state");
+    diag_kernel<<<c->diag_blocks, DIAG_NT, 0, c->stream>>>(c->kp, c->kb, c->d_part);
+    CK(cudaGetLastError());
+    std::vector<double> part((size_t)c->diag_blocks * 5);
+    CK(cudaMemcpyAsync(part.data(), c->d_part, part.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    int rc;
+    if ((rc = read_state(c))) return rc;
+    double sh = 0, sv = 0, mn = INFINITY, mx = 0, wet = 0;
+    for (int b = 0; b < c->diag_blocks; ++b) {
+        sh += part[b * 5 + 0];
+        sv += part[b * 5 + 1];
+        mn = std::fmin(mn, part[b * 5 + 2]);
+        mx = std::fmax(mx, part[b * 5 + 3]);
+        wet += part[b * 5 + 4];
+    }
+    const DevState& s = *c->h_st;
+    std::memset(d, 0, sizeof(*d));
+    d->t = s.t[c->par];
+    d->step = s.step[c->par];
+    double ax, ay;
+    std::memcpy(&ax, &s.amax[c->par][0], 8);
+    std::memcpy(&ay, &s.amax[c->par][1], 8);
+    double dt = c->p.cfl / (ax / c->p.dx + ay / c->p.dy);
+    d->dt_next = std::fmin(dt, c->p.dt_max);
+    d->volume = sh * c->p.dx * c->p.dy;
+    d->vinf_volume = sv * c->p.dx * c->p.dy;
+    d->h_min = mn;
+    d->h_max = mx;
+    d->wet_cells = (int64_t)wet;
+    d->clamps = (int64_t)s.clamps;
+    d->clamped_mass = s.clamped_mass;
+    std::memcpy(&d->clamp_max, &s.clamp_max_bits, 8);
+    d->flags = s.flags;
+    d->big_clamp_cell = s.big_clamp_cell;
+    d->big_clamp_step = s.big_clamp_step;
+    return SWOF_OK;
+}
+
+int swof_predictor(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf) {
+    if (!c) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_predictor before swof_set_state");
+    // the predictor zeroes the other parity's maxima; keep a copy so the state is left untouched
+    DevState saved;
+    int rc;
+    if ((rc = read_state(c))) return rc;
+    saved = *c->h_st;
+    stage_kernel<false><<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+    CK(cudaGetLastError());
+    if (h && (rc = copy_field_out(c, h, c->kb.Bh))) return rc;
+    if (hu && (rc = copy_field_out(c, hu, c->kb.Bhu))) return rc;
+    if (hv && (rc = copy_field_out(c, hv, c->kb.Bhv))) return rc;
+    if (v_inf && c->kp.ga && (rc = copy_field_out(c, v_inf, c->kb.VB))) return rc;
+    *c->h_st = saved;
+    CK(cudaMemcpyAsync(c->kb.st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SWOF_OK;
+}
+
+int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms) {
+    if (!c || !ms || nsteps < 0) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_step_profiled before swof_set_state");
+    const double inf = INFINITY;
+    const long long lim = INT64_MAX;
+    CK(cudaMemcpyAsync(&c->kb.st->t_end, &inf, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(&c->kb.st->step_limit, &lim, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    cudaEvent_t ev[3];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    double acc[2] = {0, 0};
+    for (int64_t n = 0; n < nsteps; ++n) {
+        CK(cudaEventRecord(ev[0], c->stream));
+        stage_kernel<false><<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+        CK(cudaEventRecord(ev[1], c->stream));
+        stage_kernel<true><<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+        CK(cudaEventRecord(ev[2], c->stream));
+        c->par ^= 1;
+        CK(cudaEventSynchronize(ev[2]));
+        float a, b;
+        CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        CK(cudaEventElapsedTime(&b, ev[1], ev[2]));
+        acc[0] += a;
+        acc[1] += b;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    ms[0] = acc[0];
+    ms[1] = acc[1];
+    int rc;
+    if ((rc = read_state(c))) return rc;
+    return flags_rc(c);
+}
+
+void swof_destroy(swof_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->own_ws && c->ws) cudaFree(c->ws);
+    if (c->h_st) cudaFreeHost(c->h_st);
+    delete c;
+}
+
+}  // extern "C"
