@@ -34,6 +34,7 @@ struct swof_ctx {
     double* d_part = nullptr;          // diag partials
     int diag_blocks = 0;
     dim3 grid;
+    StageFn kpred = nullptr, kcorr = nullptr;   // stage kernel instances for this context's physics
     std::string err;
 };
 
@@ -123,8 +124,8 @@ int cuda_fail(swof_ctx* c, cudaError_t e, const char* where) {
     } while (0)
 
 void launch_step(swof_ctx* c, int par, cudaStream_t s) {
-    stage_kernel<false><<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
-    stage_kernel<true><<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
+    c->kpred<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
+    c->kcorr<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
 }
 void launch_step(swof_ctx* c, int par) { launch_step(c, par, c->stream); }
 
@@ -296,9 +297,12 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     c->grid = dim3((unsigned)((p->nx + TX - 1) / TX), (unsigned)((p->ny + TY - 1) / TY));
     c->diag_blocks = DIAG_BLOCKS;
 
-    cudaError_t e = cudaFuncSetAttribute(stage_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(stage_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    const int fk = p->fric_law == SWOF_FRIC_NONE ? 0
+                 : (p->fric_law == SWOF_FRIC_MANNING || p->fric_law == SWOF_FRIC_STRICKLER) ? 1 : 2;
+    c->kpred = select_stage<false>(fk, k.ga != 0, has_ff);
+    c->kcorr = select_stage<true>(fk, k.ga != 0, has_ff);
+    cudaError_t e = cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->ws, 0, L.total, c->stream);
     if (e != cudaSuccess) { int rc = cuda_fail(c, e, "swof_create"); fprintf(stderr, "swof: %s\n", c->err.c_str()); swof_destroy(c); return rc; }
     int rc = copy_field_in(c, b.z, z);
@@ -468,7 +472,7 @@ int swof_predictor(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf
     int rc;
     if ((rc = read_state(c))) return rc;
     saved = *c->h_st;
-    stage_kernel<false><<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+    c->kpred<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
     CK(cudaGetLastError());
     if (h && (rc = copy_field_out(c, h, c->kb.Bh))) return rc;
     if (hu && (rc = copy_field_out(c, hu, c->kb.Bhu))) return rc;
@@ -492,9 +496,9 @@ int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms) {
     double acc[2] = {0, 0};
     for (int64_t n = 0; n < nsteps; ++n) {
         CK(cudaEventRecord(ev[0], c->stream));
-        stage_kernel<false><<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+        c->kpred<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
         CK(cudaEventRecord(ev[1], c->stream));
-        stage_kernel<true><<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+        c->kcorr<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
         CK(cudaEventRecord(ev[2], c->stream));
         c->par ^= 1;
         CK(cudaEventSynchronize(ev[2]));

@@ -39,6 +39,9 @@ constexpr int QN = (TY + NW - 1) / NW; // own rows per warp (2)
 constexpr size_t SMEM_BYTES = sizeof(double2) * (2 * NLOAD + TX * TY + 2 * NSL + 2 * NFC) + sizeof(double) * (NLOAD + TX * TY);
 static_assert(TY == 2 * NW, "two own rows per warp");
 static_assert(XSW <= 32, "x-slope row must fit one warp");
+#ifndef SWOF_FUSE_P34
+#define SWOF_FUSE_P34 1                // Fc_x in P1, so P3 (x update) and P4 (y slopes) share a phase
+#endif
 #ifndef SWOF_MIN_BLOCKS
 #define SWOF_MIN_BLOCKS 3              // CTAs per SM the register allocation must allow
 #endif
@@ -322,6 +325,15 @@ __device__ __forceinline__ FaceIn recon_minus(const double2 he, double un, doubl
     f.n = un - a * sb.x;
     f.t = ut - a * sb.y;
     return f;
+}
+
+// Fc_i = -g (h_{i-1/2+} + h_{i+1/2-})/2 (z_{i+1/2-} - z_{i-1/2+}) from the cell's {h, eta}
+// and half-slopes {dh, de}, evaluated as (g/2 (h_m + h_p)) (z_m - z_p)
+__device__ __forceinline__ double centred_source(double g2, double h, double e, double dh, double de) {
+    const double hm = h - dh, hp = h + dh;
+    const double em = e - de, ep = e + de;
+    const double zm = em - hm, zp = ep - hp;
+    return (g2 * (hm + hp)) * (zm - zp);
 }
 
 __device__ __forceinline__ double2 half_slopes(double am, double ac, double ap, double bm, double bc, double bp) {
@@ -684,6 +696,13 @@ __global__ void __launch_bounds__(NT, SWOF_MIN_BLOCKS) stage_kernel(const KParam
         s_sb[k0] = half_slopes(d0.x, e0.x, f0.x, d0.y, e0.y, f0.y);     // normal u, transverse v
         s_sa[k1] = half_slopes(a1.x, c1.x, b1.x, a1.y, c1.y, b1.y);
         s_sb[k1] = half_slopes(d1.x, e1.x, f1.x, d1.y, e1.y, f1.y);
+#if SWOF_FUSE_P34
+        if (lane >= 1 && lane <= TX) {                   // own cells: the x centred source Fc_x,
+            const double2 sl0 = s_sa[k0], sl1 = s_sa[k1];  // stashed so P3 needs no slopes (P3/P4 fuse)
+            s_pxm[warp * TX + lane - 1] = centred_source(0.5 * P.g, c0.x, c0.y, sl0.x, sl0.y);
+            s_pxm[(warp + NW) * TX + lane - 1] = centred_source(0.5 * P.g, c1.x, c1.y, sl1.x, sl1.y);
+        }
+#endif
     }
     __syncthreads();
 
@@ -711,19 +730,22 @@ __global__ void __launch_bounds__(NT, SWOF_MIN_BLOCKS) stage_kernel(const KParam
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const int r = warp + q * NW;
+#if SWOF_FUSE_P34
+            const double Fc = s_pxm[r * TX + lane];          // from P1
+#else
             const int m = (r + HALO) * LW + lane + HALO;
             const double2 he = s_he[m], sl = s_sa[r * XSW + lane + 1];
-            const double hm = he.x - sl.x, hp = he.x + sl.x;
-            const double em = he.y - sl.y, ep = he.y + sl.y;
-            const double zm = em - hm, zp = ep - hp;
-            const double Fc = (g2 * (hm + hp)) * (zm - zp);
+            const double Fc = centred_source(g2, he.x, he.y, sl.x, sl.y);
+#endif
             const int fw = r * XFW + lane;
             const double2 wa = s_fa[fw], ea = s_fa[fw + 1], wb = s_fb[fw], eb = s_fb[fw + 1];
             s_pxm[r * TX + lane] = lx * (ea.x - wa.x);
             s_q[r * TX + lane] = make_double2(lx * ((ea.y - wb.x) - Fc), lx * (eb.y - wb.y));
         }
     }
+#if !SWOF_FUSE_P34
     __syncthreads();
+#endif
 
     // ---- P4: y-axis half-slopes, rows -1..TY, own columns (normal velocity v, transverse u) ----
     if (lane < TX) {
