@@ -34,7 +34,13 @@ class OrParams(C.Structure):
         ("n_rain", C.c_int32), ("rain_t", C.c_double * MAXT), ("rain_rate", C.c_double * MAXT),
         ("bc", C.c_int32 * 4), ("in_k0", C.c_int32 * 4), ("in_k1", C.c_int32 * 4), ("n_hydro", C.c_int32 * 4),
         ("hydro_t", (C.c_double * MAXT) * 4), ("hydro_q", (C.c_double * MAXT) * 4),
+        ("flux", C.c_int32), ("order", C.c_int32), ("cfl_mode", C.c_int32), ("ga_form", C.c_int32),
     ]
+
+
+FLUX = {"hll": 0, "rusanov": 1}
+CFL_MODE = {"cell": 0, "face": 1}
+GA_FORM = {"printed": 0, "darcy": 1}
 
 
 class Counters(C.Structure):
@@ -83,6 +89,10 @@ def lib():
         L.or_centered_source.argtypes = [C.c_double] * 5
         L.or_face.restype = C.c_int
         L.or_face.argtypes = [C.c_double, C.c_double, _D, _D, _D]
+        L.or_face_rusanov.restype = C.c_int
+        L.or_face_rusanov.argtypes = [C.c_double, C.c_double, _D, _D, _D]
+        L.or_cfl_dt_face.restype = C.c_double
+        L.or_cfl_dt_face.argtypes = [P, _D, _D, _D, _D, C.c_double, C.c_double, C.c_double, _D, _D]
         L.or_green_ampt.restype = None
         L.or_green_ampt.argtypes = [P, C.c_double, C.c_double, C.c_double, _D, _D]
         L.or_friction.restype = None
@@ -136,6 +146,10 @@ def params_from_config(cfg) -> OrParams:
             P.n_hydro[s] = len(fl.hydro_t)
             for k, (t, q) in enumerate(zip(fl.hydro_t, fl.hydro_q)):
                 P.hydro_t[s][k], P.hydro_q[s][k] = t, q
+    P.flux = FLUX[getattr(cfg, "flux", "hll")]
+    P.order = int(getattr(cfg, "order", 2))
+    P.cfl_mode = CFL_MODE[getattr(cfg, "cfl_mode", "cell")]
+    P.ga_form = GA_FORM[getattr(cfg, "ga_form", "printed")]
     return P
 
 
@@ -179,6 +193,15 @@ def face(l, r, g=9.81, h_eps=1e-12):
     return d
 
 
+def face_rusanov(l, r, g=9.81, h_eps=1e-12):
+    """Rusanov face: same inputs as face(); out c = the wave-speed bound."""
+    out = np.zeros(9)
+    br = lib().or_face_rusanov(g, h_eps, _p(_arr(l)), _p(_arr(r)), _p(out))
+    d = dict(zip(("Fm", "Fn", "Ft", "SL", "SR", "HL", "HR", "c", "_"), out))
+    d["branch"] = br
+    return d
+
+
 def green_ampt(P, h_r, V, dt):
     ho, vo = C.c_double(), C.c_double()
     lib().or_green_ampt(C.byref(P), h_r, V, dt, C.byref(ho), C.byref(vo))
@@ -201,6 +224,13 @@ def pairwise_sum(x):
 def cfl_dt(P, h, hu, hv, t=0.0, t_end=float("inf")):
     ax, ay = C.c_double(), C.c_double()
     dt = lib().or_cfl_dt(C.byref(P), _p(_arr(h)), _p(_arr(hu)), _p(_arr(hv)), t, t_end, C.byref(ax), C.byref(ay))
+    return dt, ax.value, ay.value
+
+
+def cfl_dt_face(P, z, h, hu, hv, t_ghost=0.0, t=0.0, t_end=float("inf")):
+    ax, ay = C.c_double(), C.c_double()
+    dt = lib().or_cfl_dt_face(C.byref(P), _p(_arr(z)), _p(_arr(h)), _p(_arr(hu)), _p(_arr(hv)), t_ghost, t, t_end,
+                              C.byref(ax), C.byref(ay))
     return dt, ax.value, ay.value
 
 

@@ -94,12 +94,25 @@ double or_friction_gcf(int law, double coef, double g) {
  * Reconstructed variables h, h+z, u, v; z deduced as eta - h (Q3).
  * Velocity modification: u_{i-1/2+} = u_i - (h_{i+1/2-}/h_i) delta_u and
  * u_{i+1/2-} = u_i + (h_{i-1/2+}/h_i) delta_u; on dry cells both faces take u_i (Q5). */
+/* order 1 (first-order scheme): no reconstruction, every slope is 0, so each face carries the
+ * cell value (z_face = eta - h as at second order) */
+static void muscl_cell_ord(const double h3[3], const double eta3[3], const double u3[3], const double v3[3],
+                           double rh_c, int order, double out[10]);
+
 void or_muscl_cell(const double h3[3], const double eta3[3], const double u3[3], const double v3[3],
                    double rh_c, double out[10]) {
-    double dh = 0.5 * or_minmod(h3[1] - h3[0], h3[2] - h3[1]);
-    double de = 0.5 * or_minmod(eta3[1] - eta3[0], eta3[2] - eta3[1]);
-    double du = 0.5 * or_minmod(u3[1] - u3[0], u3[2] - u3[1]);
-    double dv = 0.5 * or_minmod(v3[1] - v3[0], v3[2] - v3[1]);
+    muscl_cell_ord(h3, eta3, u3, v3, rh_c, 2, out);
+}
+
+static void muscl_cell_ord(const double h3[3], const double eta3[3], const double u3[3], const double v3[3],
+                           double rh_c, int order, double out[10]) {
+    double dh = 0.0, de = 0.0, du = 0.0, dv = 0.0;
+    if (order != 1) {
+        dh = 0.5 * or_minmod(h3[1] - h3[0], h3[2] - h3[1]);
+        de = 0.5 * or_minmod(eta3[1] - eta3[0], eta3[2] - eta3[1]);
+        du = 0.5 * or_minmod(u3[1] - u3[0], u3[2] - u3[1]);
+        dv = 0.5 * or_minmod(v3[1] - v3[0], v3[2] - v3[1]);
+    }
     double hm = h3[1] - dh, hp = h3[1] + dh;
     double em = eta3[1] - de, ep = eta3[1] + de;
     double zm = em - hm, zp = ep - hp; /* z deduced as eta - h on each face */
@@ -152,6 +165,27 @@ static int hll(double g, double h_eps, double HL, double nl, double tl, double H
     return 3;
 }
 
+/* Rusanov numerical flux (P:302 names it; textbook local Lax-Friedrichs form) on the same
+ * U = (H, H*un, H*ut): F = (F(U_L) + F(U_R))/2 - (c/2)(U_R - U_L) with the single wave-speed bound
+ * c = max(|un_L| + sqrt(g H_L), |un_R| + sqrt(g H_R)).  Dry-dry face -> zero flux (as Q8). */
+static int rusanov(double g, double h_eps, double HL, double nl, double tl, double HR, double nr, double tr,
+                   double F[3], double* co) {
+    *co = 0.0;
+    if (HL <= h_eps && HR <= h_eps) { F[0] = F[1] = F[2] = 0.0; return 0; }
+    double g2 = 0.5 * g;
+    double qL = HL * nl, pL = HL * tl;
+    double qR = HR * nr, pR = HR * tr;
+    double cL = sqrt(g * HL), cR = sqrt(g * HR);
+    double c = dmax(fabs(nl) + cL, fabs(nr) + cR);
+    *co = c;
+    double FL[3] = {qL, qL * nl + g2 * (HL * HL), qL * tl};
+    double FR[3] = {qR, qR * nr + g2 * (HR * HR), qR * tr};
+    double UL[3] = {HL, qL, pL}, UR[3] = {HR, qR, pR};
+    double hc = 0.5 * c;
+    for (int k = 0; k < 3; ++k) F[k] = 0.5 * (FL[k] + FR[k]) - hc * (UR[k] - UL[k]);
+    return 3;
+}
+
 /* interface source corrections S_{i+1/2L}, S_{i-1/2R} */
 static void iface_sources(double g, double hl, double HL, double hr, double HR, double* SL, double* SR) {
     double g2 = 0.5 * g;
@@ -175,13 +209,27 @@ int or_face(double g, double h_eps, const double l[5], const double r[5], double
     return br;
 }
 
+int or_face_rusanov(double g, double h_eps, const double l[5], const double r[5], double out[9]) {
+    double zs, HL, HR, F[3], c, SL, SR;
+    hydrostatic(l, r, &zs, &HL, &HR);
+    int br = rusanov(g, h_eps, HL, l[3], l[4], HR, r[3], r[4], F, &c);
+    iface_sources(g, l[0], HL, r[0], HR, &SL, &SR);
+    out[0] = F[0]; out[1] = F[1]; out[2] = F[2]; out[3] = SL; out[4] = SR;
+    out[5] = HL; out[6] = HR; out[7] = c; out[8] = 0.0;
+    return br;
+}
+
 /* modified Green-Ampt: I_C = K_s (A + (h_f - h_over)/Z_f), Z_f = V/dtheta, read as
  * K_s (A + ((h_f - h_over) dtheta)/V), clamped >= 0; infiltrated depth min(h_over, dt I_C);
  * V = 0 -> unlimited capacity (limit of the printed formula, Q15). */
 void or_green_ampt(const or_params* P, double h_r, double V, double dt, double* h_out, double* V_out) {
     double cap;
     if (V == 0.0) cap = INFINITY;
-    else cap = dmax(P->ga_Ks * (P->ga_A + ((P->ga_hf - h_r) * P->ga_dtheta) / V), 0.0) * dt;
+    else {
+        /* as printed: h_f - h_over; the Darcy-consistent switch (Q15) takes h_f + h_over */
+        double dh = (P->ga_form == OR_GA_DARCY) ? P->ga_hf + h_r : P->ga_hf - h_r;
+        cap = dmax(P->ga_Ks * (P->ga_A + (dh * P->ga_dtheta) / V), 0.0) * dt;
+    }
     double inf = dmin(h_r, cap);
     *h_out = h_r - inf;
     *V_out = V + inf;
@@ -356,7 +404,7 @@ static void primitives(const or_params* P, ws_t* W) {
         }
 }
 
-static void muscl_axis(ws_t* W, int axis) {
+static void muscl_axis(ws_t* W, int axis, int order) {
     /* axis 0: x (neighbours i-1, i+1; normal velocity u); axis 1: y (j-1, j+1; normal velocity v) */
     int nx = W->nx, ny = W->ny;
     int i0 = axis == 0 ? -1 : 0, i1 = axis == 0 ? nx + 1 : nx;
@@ -372,7 +420,7 @@ static void muscl_axis(ws_t* W, int axis) {
             double n3[3] = {un[c - st], un[c], un[c + st]};
             double t3[3] = {ut[c - st], ut[c], ut[c + st]};
             double out[10];
-            or_muscl_cell(h3, e3, n3, t3, W->rh[c], out);
+            muscl_cell_ord(h3, e3, n3, t3, W->rh[c], order, out);
             for (int k = 0; k < 10; ++k) W->rec[axis][k][c] = out[k];
         }
 }
@@ -420,7 +468,9 @@ static void flux_axis(const or_params* P, ws_t* W, int axis, or_counters* C) {
             double l[5], r[5], F[3], c1, c2;
             face_lr(W, axis, f, row, l, r);
             size_t k = axis == 0 ? (size_t)row * nf + f : (size_t)f * nr + row;
-            int br = hll(P->g, P->h_eps, HL[k], l[3], l[4], HR[k], r[3], r[4], F, &c1, &c2);
+            int br = (P->flux == OR_FLUX_RUSANOV)
+                         ? rusanov(P->g, P->h_eps, HL[k], l[3], l[4], HR[k], r[3], r[4], F, &c1)
+                         : hll(P->g, P->h_eps, HL[k], l[3], l[4], HR[k], r[3], r[4], F, &c1, &c2);
             iface_sources(P->g, l[0], HL[k], r[0], HR[k], &SL[k], &SR[k]);
             Fm[k] = F[0]; Fn[k] = F[1]; Ft[k] = F[2];
             if (C) {
@@ -516,8 +566,8 @@ static void stage_ws(const or_params* P, ws_t* W, const double* z, const double*
     load_padded(W, z, h, hu, hv);
     fill_ghosts(P, W, t_s);               /* Boundary Conditions */
     primitives(P, W);                     /* Second order reconstruction */
-    muscl_axis(W, 0);
-    muscl_axis(W, 1);
+    muscl_axis(W, 0, P->order);
+    muscl_axis(W, 1, P->order);
     hydrostatic_axis(W, 0);               /* Hydrostatic reconstruction */
     hydrostatic_axis(W, 1);
     flux_axis(P, W, 0, C);                /* Numerical flux computation */
@@ -550,6 +600,19 @@ static void heun_ws(const or_params* P, ws_t* W, const double* z, const double* 
         hu[c] = 0.5 * (hu[c] + W->U2hu[c]);
         hv[c] = 0.5 * (hv[c] + W->U2hv[c]);
         if (P->ga_enabled) v[c] = 0.5 * (v[c] + W->U2v[c]);
+    }
+}
+
+/* explicit Euler for the first-order scheme (order 1): U^{n+1} = S(U^n; t^n) */
+static void euler_ws(const or_params* P, ws_t* W, const double* z, const double* fric,
+                     double* h, double* hu, double* hv, double* v, double t, double dt, or_counters* C) {
+    size_t n = (size_t)P->nx * P->ny;
+    stage_ws(P, W, z, fric, h, hu, hv, v, t, dt, W->U1h, W->U1hu, W->U1hv, W->U1v, C);
+    for (size_t c = 0; c < n; ++c) {
+        h[c] = W->U1h[c];
+        hu[c] = W->U1hu[c];
+        hv[c] = W->U1hv[c];
+        if (P->ga_enabled) v[c] = W->U1v[c];
     }
 }
 
@@ -586,6 +649,41 @@ double or_cfl_dt(const or_params* P, const double* h, const double* hu, const do
     return dt;
 }
 
+/* CFL on the reconstructed values: "at second order, variables (h_i, u_i) in (cfl) are
+ * replaced by the reconstructed values".  Read (Q22) as: every cell contributes the speeds of
+ * its own two face reconstructions per axis, |u_{i-1/2+}| + sqrt(g h_{i-1/2+}) and
+ * |u_{i+1/2-}| + sqrt(g h_{i+1/2-}) (MUSCL values with the velocity modification, before the
+ * hydrostatic reconstruction; ghosts at t_ghost feed the slopes of the edge cells).  At order 1 the
+ * faces carry the cell values, so this equals or_cfl_dt. */
+double or_cfl_dt_face(const or_params* P, const double* z, const double* h, const double* hu, const double* hv,
+                      double t_ghost, double t, double t_end, double* axo, double* ayo) {
+    ws_t W;
+    if (ws_alloc(&W, P->nx, P->ny)) { ws_free(&W); return NAN; }
+    load_padded(&W, z, h, hu, hv);
+    fill_ghosts(P, &W, t_ghost);
+    primitives(P, &W);
+    muscl_axis(&W, 0, P->order);
+    muscl_axis(&W, 1, P->order);
+    double a[2] = {0.0, 0.0};
+    for (int axis = 0; axis < 2; ++axis)
+        for (int j = 0; j < P->ny; ++j)
+            for (int i = 0; i < P->nx; ++i) {
+                size_t c = PIX(&W, i, j);
+                double* const* R = W.rec[axis];
+                double sm = fabs(R[R_NM][c]) + sqrt(P->g * R[R_HM][c]);
+                double sp = fabs(R[R_NP][c]) + sqrt(P->g * R[R_HP][c]);
+                if (sm > a[axis] || sm != sm) a[axis] = sm;
+                if (sp > a[axis] || sp != sp) a[axis] = sp;
+            }
+    ws_free(&W);
+    if (axo) *axo = a[0];
+    if (ayo) *ayo = a[1];
+    double dt = P->cfl / (a[0] / P->dx + a[1] / P->dy);
+    dt = dmin(dt, P->dt_max);
+    dt = dmin(dt, t_end - t);
+    return dt;
+}
+
 int or_run(const or_params* P, const double* z, const double* fric,
            double* h, double* hu, double* hv, double* v,
            double* t, int64_t nsteps, double t_end, double dt_forced,
@@ -596,9 +694,12 @@ int or_run(const or_params* P, const double* z, const double* fric,
     int rc = 0;
     for (; n < nsteps; ++n) {
         if (*t >= t_end) break;
-        double dt = dt_forced > 0.0 ? dt_forced : or_cfl_dt(P, h, hu, hv, *t, t_end, NULL, NULL);
+        double dt = dt_forced > 0.0 ? dt_forced
+                  : (P->cfl_mode == OR_CFL_FACE) ? or_cfl_dt_face(P, z, h, hu, hv, *t, *t, t_end, NULL, NULL)
+                  : or_cfl_dt(P, h, hu, hv, *t, t_end, NULL, NULL);
         if (!isfinite(dt) || !(dt > 0.0)) { rc = -2; break; }
-        heun_ws(P, &W, z, fric, h, hu, hv, v, *t, dt, C);
+        if (P->order == 1) euler_ws(P, &W, z, fric, h, hu, hv, v, *t, dt, C);
+        else heun_ws(P, &W, z, fric, h, hu, hv, v, *t, dt, C);
         *t = *t + dt;
         if (dt_hist && n < cap) dt_hist[n] = dt;
     }

@@ -27,6 +27,10 @@ extern "C" {
 enum { OR_FRIC_NONE = 0, OR_FRIC_MANNING = 1, OR_FRIC_STRICKLER = 2, OR_FRIC_DARCY = 3, OR_FRIC_CHEZY = 4 };
 enum { OR_BC_WALL = 0, OR_BC_FREE = 1, OR_BC_PERIODIC = 2, OR_BC_INFLOW = 3 };
 enum { OR_W = 0, OR_E = 1, OR_S = 2, OR_N = 3 };
+/* scheme variants; the zero values are the default scheme */
+enum { OR_FLUX_HLL = 0, OR_FLUX_RUSANOV = 1 };       /* numerical flux */
+enum { OR_CFL_CELL = 0, OR_CFL_FACE = 1 };           /* CFL on cell values or reconstructed values */
+enum { OR_GA_PRINTED = 0, OR_GA_DARCY = 1 };         /* Green-Ampt h_over sign (Q15) */
 #define OR_MAX_TABLE 16
 
 typedef struct {
@@ -43,6 +47,10 @@ typedef struct {
     int32_t in_k0[4], in_k1[4];  /* inflow segment [k0, k1) per side */
     int32_t n_hydro[4];
     double hydro_t[4][OR_MAX_TABLE], hydro_q[4][OR_MAX_TABLE];
+    int32_t flux;                /* OR_FLUX_*                                                      */
+    int32_t order;               /* 2 (or 0): MUSCL + Heun; 1: first order in space, explicit Euler */
+    int32_t cfl_mode;            /* OR_CFL_*                                                       */
+    int32_t ga_form;             /* OR_GA_*                                                        */
 } or_params;
 
 /* per-run counters (used for the algorithmic op count F_alg and the clamp audit) */
@@ -72,6 +80,9 @@ void or_muscl_cell(const double h3[3], const double eta3[3], const double u3[3],
    out[9] = Fm, Fn, Ft, S_L, S_R, H_L, H_R, c1, c2 ; returns branch 0 dry, 1 left, 2 right, 3 middle */
 double or_centered_source(double g, double hm, double hp, double zm, double zp);
 int or_face(double g, double h_eps, const double l[5], const double r[5], double out[9]);
+/* the same with the Rusanov flux (textbook local Lax-Friedrichs): F = (F_L + F_R)/2 - c/2 (U_R - U_L),
+   c = max(|un_L| + sqrt(g H_L), |un_R| + sqrt(g H_R)); out[7] = c, out[8] = 0; returns 0 dry, 3 otherwise */
+int or_face_rusanov(double g, double h_eps, const double l[5], const double r[5], double out[9]);
 /* Green-Ampt for one cell: in h_r (post-rain height), V, dt; out h*, V' */
 void or_green_ampt(const or_params* P, double h_r, double V, double dt, double* h_out, double* V_out);
 /* semi-implicit friction on one cell; state s = stage input, (hs,hus,hvs); (hst,hup,hvp) post-source */
@@ -82,6 +93,11 @@ void or_friction(double gcf, int law, double h_eps, double dt, double hs, double
 /* CFL (Q10/Q17): dt = min(cfl/(ax/dx + ay/dy), dt_max, t_end - t). Writes ax, ay if non-NULL. */
 double or_cfl_dt(const or_params* P, const double* h, const double* hu, const double* hv,
                  double t, double t_end, double* ax, double* ay);
+/* CFL on reconstructed values (reading Q22): a_x = max over cells of the speeds
+   |u| + sqrt(g h) of the cell's two x-face reconstructions (h_{i-1/2+}, u_{i-1/2+}), (h_{i+1/2-}, u_{i+1/2-})
+   (ghosts filled at t_ghost), a_y likewise; dt as or_cfl_dt. */
+double or_cfl_dt_face(const or_params* P, const double* z, const double* h, const double* hu, const double* hv,
+                      double t_ghost, double t, double t_end, double* ax, double* ay);
 /* one stage S(U, V; t_s, dt) of SURVEY.md §8c c1. v_in/v_out may be NULL if GA disabled.
    fric may be NULL (scalar coefficient). */
 int or_stage(const or_params* P, const double* z, const double* fric,
@@ -91,7 +107,7 @@ int or_stage(const or_params* P, const double* z, const double* fric,
 /* one Heun step in place, with the given dt (t = t^n). */
 int or_heun_step(const or_params* P, const double* z, const double* fric,
                  double* h, double* hu, double* hv, double* v, double t, double dt, or_counters* C);
-/* time loop: nsteps Heun steps (or until t >= t_end), dt from the CFL of the current state unless
+/* time loop: nsteps steps (Heun; explicit Euler when order == 1) (or until t >= t_end), dt from the CFL of the current state unless
    dt_forced > 0.  dt_hist (capacity cap) receives every dt.  Returns 0 or a negative error. */
 int or_run(const or_params* P, const double* z, const double* fric,
            double* h, double* hu, double* hv, double* v,

@@ -62,6 +62,11 @@ class SwofConfig:
     rain_rate: list = field(default_factory=list)  # m/s
     bc: dict = field(default_factory=lambda: {s: "wall" for s in SIDES})
     inflow: dict = field(default_factory=dict)     # side -> Inflow
+    # scheme variants; the defaults are the paper's recommended scheme
+    flux: str = "hll"                              # "hll" | "rusanov"
+    order: int = 2                                 # 2: MUSCL + Heun | 1: first order, explicit Euler
+    cfl_mode: str = "cell"                         # "cell" (Q10) | "face": reconstructed values
+    ga_form: str = "printed"                       # "printed" | "darcy": h_f + h_over (Q15)
     steps: Optional[int] = None                    # fixed step count (swof_step), or
     t_end: Optional[float] = None                  # run to t_end (swof_run)
     # inputs
