@@ -198,6 +198,7 @@ def main():
     cells = cfg.nx * cfg.ny
     stream = torch.cuda.Stream()
     solver = Solver(params_from_config(cfg), cfg.z, cfg.fric_field, stream=stream)
+    launches_per_step = solver.launches_per_step()
     v0 = cfg.vinf if cfg.ga is not None else None
     solver.set_state(cfg.h, cfg.hu, cfg.hv, v0, 0.0)
 
@@ -272,7 +273,7 @@ def main():
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                    "l2": "inputs (>=4.6 GB of fields) larger than L2; no flush"},
         "e2e": e2e,
-        "gpu_launches": args.steps * Solver.launches_per_step(),
+        "gpu_launches": args.steps * launches_per_step,
         "kernels_ms": {"predictor": ms_pred, "corrector": ms_corr},
         "hbm": {"dominant_kernel": dom, "achieved_gbs": hbm_achieved, "peak_gbs": peaks["hbm_gbs"],
                 "frac": hbm_achieved / peaks["hbm_gbs"], "bytes_per_cell_update": bp + bc, "peak_source": src},

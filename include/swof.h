@@ -52,6 +52,15 @@ extern "C" {
 #define SWOF_BC_PERIODIC 2  /* wrap (both opposite sides must be PERIODIC)                      */
 #define SWOF_BC_INFLOW 3    /* imposed (h_c(q), q = Q(t)/W, 0) on [k0, k1), WALL elsewhere        */
 
+/* scheme variants; zero-initialised params give the paper's recommended
+ * scheme: HLL, second order (MUSCL + Heun), CFL on cell-centred speeds, Green-Ampt as printed */
+#define SWOF_FLUX_HLL 0
+#define SWOF_FLUX_RUSANOV 1  /* F = (F_L + F_R)/2 - c/2 (U_R - U_L), c = max(|u| + sqrt(g h)) */
+#define SWOF_CFL_CELL 0      /* a = max over cells of |u| + sqrt(g h) (Q10)               */
+#define SWOF_CFL_FACE 1      /* over every cell's reconstructed face values (Q22)        */
+#define SWOF_GA_PRINTED 0    /* I_C = K_s (A + (h_f - h_over)/Z_f)                           */
+#define SWOF_GA_DARCY 1      /* I_C = K_s (A + (h_f + h_over)/Z_f) (Q15)                            */
+
 #define SWOF_SIDE_W 0
 #define SWOF_SIDE_E 1
 #define SWOF_SIDE_S 2
@@ -91,6 +100,11 @@ typedef struct swof_params {
     int32_t graph_steps;     /* Heun steps per captured CUDA graph (0 -> 16; rounded up to even)  */
     double clamp_fail;       /* a single negative-height clamp above this [m] raises SWOF_FLAG_BIGCLAMP
                                 and SWOF_ENUMERIC (0 -> 1e-6 m; DESIGN.md §3 Q17)                  */
+    int32_t flux;            /* SWOF_FLUX_*                                                       */
+    int32_t order;           /* 2 (or 0): MUSCL + Heun; 1: first order in
+                                space (no reconstruction) and explicit Euler in time      */
+    int32_t cfl_mode;        /* SWOF_CFL_*                                                        */
+    int32_t ga_form;         /* SWOF_GA_*                                                         */
 } swof_params;
 
 typedef struct swof_diag {
@@ -131,7 +145,8 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
 int swof_set_state(swof_ctx* c, const double* h, const double* hu, const double* hv, const double* v_inf,
                    double t0);
 
-/* Advance nsteps Heun steps with dt = min(CFL dt, dt_max) each (no t_end clipping).
+/* Advance nsteps time steps (Heun, or explicit Euler at order 1) with dt = min(CFL dt, dt_max) each
+ * (no t_end clipping).
  * Returns SWOF_ENUMERIC if a flag is set afterwards. */
 int swof_step(swof_ctx* c, int64_t nsteps);
 
@@ -151,14 +166,18 @@ int swof_get_diag(swof_ctx* c, swof_diag* d);
 
 /* Testing/profiling entry points (same kernels as swof_step):
  * swof_predictor: run only the predictor stage U* = S(U^n; t^n) of the next step and copy U*, V*
- *   out (host or device; nullable); the state is not advanced.
+ *   out (host or device; nullable); the state is not advanced (at order 1, U* is the next state).
  * swof_step_profiled: like swof_step but launched eagerly with CUDA events around every kernel;
- *   ms[0], ms[1] receive the summed device time of the predictor and corrector kernels. */
+ *   ms[0], ms[1] receive the summed device time of the predictor and of the rest of the step
+ *   (corrector, or the order-1 commit; plus the face-CFL pass if any). */
 int swof_predictor(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf);
 int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms);
 
-/* Number of kernel launches one Heun step issues (2). */
+/* Number of kernel launches one time step issues with the default scheme (2: predictor and
+ * corrector).  swof_ctx_launches_per_step: the same for a context's scheme (2, or 3 with SWOF_CFL_FACE:
+ * the reconstructed-value CFL maxima are a separate stencil pass). */
 int swof_launches_per_step(void);
+int swof_ctx_launches_per_step(const swof_ctx* c);
 
 /* Self-test of the kernels' slow-path-free IEEE reciprocal, division and square root against CUDA's
  * library operators on n random operands (exponents in [-60, 60], sqrt in [-80, 40]) on the current

@@ -105,6 +105,10 @@ const char* validate(const swof_params* p) {
     if (p->dt_hist_cap < 0) return "dt_hist_cap must be >= 0";
     if (p->graph_steps < 0) return "graph_steps must be >= 0";
     if (!(p->clamp_fail >= 0)) return "clamp_fail must be >= 0";
+    if (p->flux != SWOF_FLUX_HLL && p->flux != SWOF_FLUX_RUSANOV) return "unknown flux";
+    if (p->order < 0 || p->order > 2) return "order must be 0 (= 2), 1 or 2";
+    if (p->cfl_mode != SWOF_CFL_CELL && p->cfl_mode != SWOF_CFL_FACE) return "unknown cfl_mode";
+    if (p->ga_form != SWOF_GA_PRINTED && p->ga_form != SWOF_GA_DARCY) return "unknown ga_form";
     return nullptr;
 }
 
@@ -123,9 +127,18 @@ int cuda_fail(swof_ctx* c, cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
     } while (0)
 
+constexpr int PW_BLOCKS = 1184;        // point-wise / face-CFL passes: 8 CTAs x 148 SMs, grid-stride
+
+// one time step: predictor stage, then the corrector (Heun) or the order-1 commit
+// (explicit Euler), then the reconstructed-value CFL pass when SWOF_CFL_FACE
+void launch_second(swof_ctx* c, int par, cudaStream_t s) {
+    if (c->kp.order == 1) euler_commit_kernel<<<PW_BLOCKS, PW_NT, 0, s>>>(c->kp, c->kb, par);
+    else c->kcorr<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
+    if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<PW_BLOCKS, PW_NT, 0, s>>>(c->kp, c->kb, par, 0);
+}
 void launch_step(swof_ctx* c, int par, cudaStream_t s) {
     c->kpred<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
-    c->kcorr<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
+    launch_second(c, par, s);
 }
 void launch_step(swof_ctx* c, int par) { launch_step(c, par, c->stream); }
 
@@ -204,6 +217,7 @@ __global__ void fill_kernel(double* a, int nx, int ny, int pitch, double v) {
 extern "C" {
 
 int swof_launches_per_step(void) { return 2; }
+int swof_ctx_launches_per_step(const swof_ctx* c) { return c ? 2 + (c->kp.cfl_mode == SWOF_CFL_FACE ? 1 : 0) : -1; }
 
 int swof_selftest_math(int64_t n, uint64_t seed, int64_t* mismatches) {
     if (n < 0 || !mismatches) return SWOF_EINVAL;
@@ -285,6 +299,12 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     k.fric_coef = p->fric_coef;
     k.clamp_fail = p->clamp_fail > 0 ? p->clamp_fail : 1e-6;
     k.Ks = p->ga_Ks; k.hf = p->ga_hf; k.A = p->ga_A; k.dtheta = p->ga_dtheta;
+    k.fk = p->fric_law == SWOF_FRIC_NONE ? 0
+         : (p->fric_law == SWOF_FRIC_MANNING || p->fric_law == SWOF_FRIC_STRICKLER) ? 1 : 2;
+    k.flux = p->flux;
+    k.order = p->order == 1 ? 1 : 2;
+    k.cfl_mode = p->cfl_mode;
+    k.ga_form = p->ga_form;
     k.n_rain = p->n_rain;
     for (int i = 0; i < p->n_rain; ++i) { k.rain_t[i] = p->rain_t[i]; k.rain_rate[i] = p->rain_rate[i]; }
     for (int s = 0; s < 4; ++s) {
@@ -297,10 +317,9 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     c->grid = dim3((unsigned)((p->nx + TX - 1) / TX), (unsigned)((p->ny + TY - 1) / TY));
     c->diag_blocks = DIAG_BLOCKS;
 
-    const int fk = p->fric_law == SWOF_FRIC_NONE ? 0
-                 : (p->fric_law == SWOF_FRIC_MANNING || p->fric_law == SWOF_FRIC_STRICKLER) ? 1 : 2;
-    c->kpred = select_stage<false>(fk, k.ga != 0, has_ff);
-    c->kcorr = select_stage<true>(fk, k.ga != 0, has_ff);
+    const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
+    c->kpred = select_stage<false>(k.fk, k.ga != 0, has_ff, generic);
+    c->kcorr = select_stage<true>(k.fk, k.ga != 0, has_ff, generic);
     cudaError_t e = cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->ws, 0, L.total, c->stream);
@@ -341,6 +360,10 @@ int swof_set_state(swof_ctx* c, const double* h, const double* hu, const double*
     *c->h_st = s;
     CK(cudaMemcpyAsync(c->kb.st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
     init_cfl_kernel<<<1184, 256, 0, c->stream>>>(c->kp, c->kb);
+    if (c->kp.cfl_mode == SWOF_CFL_FACE) {               // replace the cell maxima by the face ones
+        CK(cudaMemsetAsync(&c->kb.st->amax[0][0], 0, 2 * sizeof(unsigned long long), c->stream));
+        cfl_face_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, 0, 1);
+    }
     CK(cudaGetLastError());
     c->par = 0;
     if ((rc = read_state(c))) return rc;
@@ -498,7 +521,7 @@ int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms) {
         CK(cudaEventRecord(ev[0], c->stream));
         c->kpred<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
         CK(cudaEventRecord(ev[1], c->stream));
-        c->kcorr<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+        launch_second(c, c->par, c->stream);
         CK(cudaEventRecord(ev[2], c->stream));
         c->par ^= 1;
         CK(cudaEventSynchronize(ev[2]));

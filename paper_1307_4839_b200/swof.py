@@ -16,12 +16,16 @@ _LIB_PATH = Path(__file__).resolve().parent / "libswof.so"
 SWOF_OK, SWOF_EINVAL, SWOF_ENUMERIC, SWOF_ECUDA, SWOF_ENOMEM, SWOF_ESTATE = range(6)
 FRIC = {"none": 0, "manning": 1, "strickler": 2, "darcy_weisbach": 3, "chezy": 4}
 BC = {"wall": 0, "free": 1, "periodic": 2, "inflow": 3}
+FLUX = {"hll": 0, "rusanov": 1}
+CFL_MODE = {"cell": 0, "face": 1}
+GA_FORM = {"printed": 0, "darcy": 1}
 SIDES = ("W", "E", "S", "N")
 MAXT = 16
 FLAG_NONFINITE, FLAG_BIGCLAMP, FLAG_BADINPUT = 1, 2, 4
 EXPORTS = ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run", "swof_get_state",
            "swof_get_dt_history", "swof_get_diag", "swof_predictor", "swof_step_profiled",
-           "swof_launches_per_step", "swof_selftest_math", "swof_destroy", "swof_last_error", "swof_strerror")
+           "swof_launches_per_step", "swof_ctx_launches_per_step", "swof_selftest_math", "swof_destroy",
+           "swof_last_error", "swof_strerror")
 
 
 class SwofParams(C.Structure):
@@ -36,6 +40,7 @@ class SwofParams(C.Structure):
         ("bc", C.c_int32 * 4), ("inflow_k0", C.c_int32 * 4), ("inflow_k1", C.c_int32 * 4),
         ("n_hydro", C.c_int32 * 4), ("hydro_t", (C.c_double * MAXT) * 4), ("hydro_q", (C.c_double * MAXT) * 4),
         ("dt_hist_cap", C.c_int64), ("graph_steps", C.c_int32), ("clamp_fail", C.c_double),
+        ("flux", C.c_int32), ("order", C.c_int32), ("cfl_mode", C.c_int32), ("ga_form", C.c_int32),
     ]
 
 
@@ -81,6 +86,7 @@ def lib():
         L.swof_predictor.argtypes = [vp, dp, dp, dp, dp]
         L.swof_step_profiled.argtypes = [vp, C.c_int64, C.POINTER(C.c_double)]
         L.swof_launches_per_step.argtypes = []
+        L.swof_ctx_launches_per_step.argtypes = [vp]
         L.swof_selftest_math.argtypes = [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]
         L.swof_destroy.argtypes = [vp]
         L.swof_destroy.restype = None
@@ -90,7 +96,8 @@ def lib():
         L.swof_strerror.restype = C.c_char_p
         for name in ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run",
                      "swof_get_state", "swof_get_dt_history", "swof_get_diag", "swof_predictor",
-                     "swof_step_profiled", "swof_launches_per_step", "swof_selftest_math"):
+                     "swof_step_profiled", "swof_launches_per_step", "swof_ctx_launches_per_step",
+                     "swof_selftest_math"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -118,6 +125,11 @@ def params_from_config(cfg, graph_steps: int = 0, dt_hist_cap: int = 0) -> SwofP
                 p.hydro_t[s][k], p.hydro_q[s][k] = t, q
     p.dt_hist_cap = dt_hist_cap
     p.graph_steps = graph_steps
+    p.flux = FLUX[getattr(cfg, "flux", "hll")]
+    p.order = int(getattr(cfg, "order", 2))
+    p.cfl_mode = CFL_MODE[getattr(cfg, "cfl_mode", "cell")]
+    p.ga_form = GA_FORM[getattr(cfg, "ga_form", "printed")]
+    p.clamp_fail = float(getattr(cfg, "clamp_fail", 0.0))
     return p
 
 
@@ -236,9 +248,9 @@ class Solver:
         self._check(self._L.swof_step_profiled(self._ctx, int(nsteps), ms))
         return ms[0], ms[1]
 
-    @staticmethod
-    def launches_per_step() -> int:
-        return lib().swof_launches_per_step()
+    def launches_per_step(self) -> int:
+        """Kernel launches one time step of this context issues."""
+        return self._L.swof_ctx_launches_per_step(self._ctx)
 
 
 def selftest_math(n: int = 1 << 24, seed: int = 1307):

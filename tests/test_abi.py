@@ -43,7 +43,8 @@ def test_struct_layout_matches_header(L):
     import tempfile
     from paper_1307_4839_b200.swof import SwofDiag, SwofParams
     src = '#include "swof.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(){printf("%zu %zu %zu %zu\\n", ' \
-          'sizeof(swof_params), sizeof(swof_diag), offsetof(swof_params, graph_steps), offsetof(swof_diag, flags));}'
+          'sizeof(swof_params), sizeof(swof_diag), offsetof(swof_params, graph_steps), offsetof(swof_diag, flags));' \
+          'printf("%zu\\n", offsetof(swof_params, ga_form));}'
     with tempfile.TemporaryDirectory() as d:
         c = Path(d) / "p.c"
         c.write_text(src)
@@ -51,7 +52,7 @@ def test_struct_layout_matches_header(L):
         subprocess.run(["gcc", "-I", str(ROOT / "include"), str(c), "-o", str(exe)], check=True)
         out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
     assert [int(x) for x in out] == [C.sizeof(SwofParams), C.sizeof(SwofDiag), SwofParams.graph_steps.offset,
-                                     SwofDiag.flags.offset]
+                                     SwofDiag.flags.offset, SwofParams.ga_form.offset]
 
 
 def test_workspace_size_and_validation_on_host(L):
@@ -71,6 +72,10 @@ def test_workspace_size_and_validation_on_host(L):
     bad = params_from_config(make("cfg3", nx=64, ny=64))
     bad.inflow_k1[0] = 1000
     assert L.swof_workspace_size(C.byref(bad), C.byref(n)) == 1
+    for field, value in (("flux", 2), ("order", 3), ("cfl_mode", 2), ("ga_form", -1)):
+        bad = params_from_config(make("cfg0"))
+        setattr(bad, field, value)
+        assert L.swof_workspace_size(C.byref(bad), C.byref(n)) == 1, field
     assert L.swof_strerror(4) == b"out of memory"
 
 
