@@ -7,5 +7,5 @@ never imports it.  See oracle/swof_oracle.h for the method, citations and parity
 from .oracle import (  # noqa: F401
     build, lib, params_from_config, minmod, icbrt, muscl_cell, face, centered_source, green_ampt, friction,
     friction_gcf, rain_rate, hydrograph, cfl_dt, stage, heun_step, run, pairwise_sum, Counters,
-    face_rusanov, cfl_dt_face,
+    face_rusanov, cfl_dt_face, flow_direction,
 )

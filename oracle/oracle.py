@@ -108,6 +108,10 @@ def lib():
         L.or_run.restype = C.c_int
         L.or_run.argtypes = [P, _D, _D, _D, _D, _D, _D, _D, C.c_int64, C.c_double, C.c_double, _D,
                              C.c_int64, C.POINTER(C.c_int64), C.POINTER(Counters)]
+        L.or_flow_direction.restype = None
+        L.or_flow_direction.argtypes = [_D, C.c_int32, C.c_int32, C.c_void_p]
+        L.or_flow_direction_f32.restype = None
+        L.or_flow_direction_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         L.or_pairwise_sum.restype = C.c_double
         L.or_pairwise_sum.argtypes = [_D, C.c_int64]
         _lib = L
@@ -213,6 +217,19 @@ def friction(gcf, law, dt, hs, hus, hvs, hst, hup, hvp, h_eps=1e-12):
     lib().or_friction(gcf, FRIC[law] if isinstance(law, str) else law, h_eps, dt, hs, hus, hvs, hst, hup, hvp,
                       C.byref(a), C.byref(b))
     return a.value, b.value
+
+
+def flow_direction(z):
+    """D8 flow direction (listing P:683-708) of a (ny, nx) DEM, float64 or float32 -> uint8 0..8."""
+    z = np.ascontiguousarray(z)
+    ny, nx = z.shape
+    out = np.empty((ny, nx), dtype=np.uint8)
+    if z.dtype == np.float32:
+        lib().or_flow_direction_f32(C.c_void_p(z.ctypes.data), nx, ny, C.c_void_p(out.ctypes.data))
+    else:
+        z = _arr(z)
+        lib().or_flow_direction(_p(z), nx, ny, C.c_void_p(out.ctypes.data))
+    return out
 
 
 def pairwise_sum(x):

@@ -717,3 +717,46 @@ double or_pairwise_sum(const double* x, int64_t n) {
     int64_t m = n / 2;
     return or_pairwise_sum(x, m) + or_pairwise_sum(x + m, n - m);
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* D8 flow direction: "getting the minimum value for the eight neighbors around the */
+/* current point and saving the corresponding direction", transcribed from the listing P:683-708 */
+/* ------------------------------------------------------------------------------------------ */
+static const int D8_DI[8] = {1, 1, 0, -1, -1, -1, 0, 1};   /* E, SE, S, SW, W, NW, N, NE */
+static const int D8_DJ[8] = {0, -1, -1, -1, 0, 1, 1, 1};
+
+void or_flow_direction(const double* z, int32_t nx, int32_t ny, uint8_t* dir) {
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            int index = 0;
+            double min = z[(size_t)j * nx + i];
+            for (int k = 0; k < 8; ++k) {
+                int ii = i + D8_DI[k], jj = j + D8_DJ[k];
+                if (ii < 0 || ii >= nx || jj < 0 || jj >= ny) continue;   /* absent neighbour */
+                double n = z[(size_t)jj * nx + ii];
+                if (n > 0 && n < min) {
+                    index = k + 1;
+                    min = n;
+                }
+            }
+            dir[(size_t)j * nx + i] = (uint8_t)index;
+        }
+}
+
+void or_flow_direction_f32(const float* z, int32_t nx, int32_t ny, uint8_t* dir) {
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            int index = 0;
+            float min = z[(size_t)j * nx + i];
+            for (int k = 0; k < 8; ++k) {
+                int ii = i + D8_DI[k], jj = j + D8_DJ[k];
+                if (ii < 0 || ii >= nx || jj < 0 || jj >= ny) continue;
+                float n = z[(size_t)jj * nx + ii];
+                if (n > 0 && n < min) {
+                    index = k + 1;
+                    min = n;
+                }
+            }
+            dir[(size_t)j * nx + i] = (uint8_t)index;
+        }
+}

@@ -113,6 +113,12 @@ int or_run(const or_params* P, const double* z, const double* fric,
            double* h, double* hu, double* hv, double* v,
            double* t, int64_t nsteps, double t_end, double dt_forced,
            double* dt_hist, int64_t cap, int64_t* steps_done, or_counters* C);
+/* D8 flow direction of a DEM (the user function listed at P:683-708): per cell,
+   min = own value, index = 0; for the 8 neighbours i = 0..7 in the order E, SE, S, SW, W, NW, N, NE
+   (SPEC.md flow_direction; j grows northwards), if (n_i > 0 && n_i < min) { index = i + 1; min = n_i; }.
+   Neighbours outside the grid are absent.  dir receives 0..8. */
+void or_flow_direction(const double* z, int32_t nx, int32_t ny, uint8_t* dir);
+void or_flow_direction_f32(const float* z, int32_t nx, int32_t ny, uint8_t* dir);
 /* fixed-order pairwise sum (volume audits) */
 double or_pairwise_sum(const double* x, int64_t n);
 
