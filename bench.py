@@ -3,6 +3,7 @@
 BASELINE.json throughput/roofline configuration), fp64, 1 x B200 per rank.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg4]
+    python bench.py --workload d8 [--steps K] [--warmup W] [--d8-dtype f32|f64]
 
 N > 1 is launched by torchrun; every rank advances its own full cfg4 replica (the north star excludes
 domain decomposition: "replicas only", weak scaling, no data-path collective).  Timing: W untimed
@@ -176,14 +177,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-crop", type=int, default=1024)
     ap.add_argument("--cpu-steps", type=int, default=12)
+    ap.add_argument("--workload", default="swof", choices=("swof", "d8"))
+    ap.add_argument("--d8-dtype", default="f32", choices=("f32", "f64"))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     rank, world, local = dist_env()
     from workloads import make
-
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if args.workload == "d8":
+        return bench_d8(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -317,6 +321,101 @@ def main():
         dist.destroy_process_group()
 
 
+def bench_d8(args, rank, world, local):
+    """D8 flow direction on the paper's 14786 x 10086 DEM size, synthetic
+    seeded raster (workloads/dem.py).  One "step" = one pass over the whole raster.  HBM-bound: the
+    algorithmic bytes are one read of the raster and one code byte written per point."""
+    import torch
+    import torch.distributed as dist
+    from paper_1307_4839_b200 import flow_direction
+    from workloads.dem import DEM_SIZES, make_dem
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    nx, ny = DEM_SIZES["dem_large"]
+    npts = nx * ny
+    dtype = np.float32 if args.d8_dtype == "f32" else np.float64
+    z = make_dem(nx, ny, dtype=dtype)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        zd = torch.from_numpy(z).cuda()
+        out = torch.empty((ny, nx), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        flow_direction(zd, out, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # device-resident: K passes, raster (>= 596 MB) larger than L2 -> no flush
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev[0].record(stream)
+        for k in range(args.steps):
+            flow_direction(zd, out, stream=stream)
+            ev[k + 1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    ms = reduce_max(ev[0].elapsed_time(ev[-1]), world, "cuda")
+    value = world * npts * args.steps / (ms / 1e3)
+    # end to end: pinned host raster in, codes out, every step
+    zp = torch.from_numpy(z).pin_memory()
+    op = torch.empty((ny, nx), dtype=torch.uint8).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            zd.copy_(zp, non_blocking=True)
+        flow_direction(zd, out, stream=stream)
+        with torch.cuda.stream(stream):
+            op.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = reduce_max(e0.elapsed_time(e1), world, "cuda")
+    ok_codes = int(out.max().item()) <= 8
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks, src = load_peaks()
+    bpp = z.itemsize + 1
+    kern_ms = float(np.mean(per))
+    ach = npts * bpp / (kern_ms / 1e3) / 1e9
+    outj = {"metric": f"D8 flow-direction points/s ({args.d8_dtype} DEM, 1xB200)", "value": value, "unit": "points/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.d8_dtype,
+            "data": "synthetic (seeded sinusoid DEM, 1 cm quantised, no-data disc; workloads/dem.py)",
+            "config": {"workload": "d8 dem_large", "nx": nx, "ny": ny, "points": npts,
+                       "l2": f"raster {z.nbytes / 1e6:.0f} MB > L2; no flush"},
+            "e2e": {"value": world * npts * args.steps / (ms_e2e / 1e3), "unit": "points/s",
+                    "h2d_bytes_per_step": z.nbytes, "d2h_bytes_per_step": npts},
+            "gpu_launches": args.steps,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": ach / peaks["hbm_gbs"], "traffic": None, "algorithmic_bytes_per_point": bpp,
+                         "kernel": "d8_kernel", "peak_source": src},
+            "clocks": clk.summary(), "codes_ok": ok_codes,
+            "paper_context": "SkelGIS 31 s / SkeTo 101 s for this size on the paper's CPU cluster (P:604-612)"}
+    if not args.no_cpu_baseline:
+        import oracle
+        t0 = time.perf_counter()
+        ref = oracle.flow_direction(z)
+        secs = time.perf_counter() - t0
+        outj["cpu_baseline"] = {"value": npts / secs, "unit": "points/s", "cores": 1, "kind": "oracle",
+                                "sample": f"the whole {nx}x{ny} raster, {secs:.1f} s single-threaded"}
+        outj["parity_full_raster"] = bool(np.array_equal(ref, out.cpu().numpy()))
+    print(json.dumps(outj), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def reference_arm(args, rank, world):
     """--impl reference: the oracle (plain single-threaded C), as it stands, on the host cores; each step
     is one Heun step on a bounded crop of the workload."""
@@ -324,6 +423,27 @@ def reference_arm(args, rank, world):
         return
     import oracle
     from workloads import make
+    if args.workload == "d8":
+        from workloads.dem import DEM_SIZES, make_dem
+        nx, ny = DEM_SIZES["dem_large"]
+        z = make_dem(nx, ny, dtype=np.float32 if args.d8_dtype == "f32" else np.float64)
+        for _ in range(min(args.warmup, 1)):
+            oracle.flow_direction(z)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.flow_direction(z)
+        secs = time.perf_counter() - t0
+        rate = nx * ny * args.steps / secs
+        print(json.dumps({"metric": f"D8 flow-direction points/s ({args.d8_dtype} DEM, 1xB200)", "value": rate,
+                          "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": args.d8_dtype, "data": "synthetic",
+                          "config": {"workload": "d8 dem_large", "nx": nx, "ny": ny}, "impl": "reference",
+                          "cpu_baseline": {"value": rate, "unit": "points/s", "cores": 1, "kind": "oracle",
+                                           "sample": f"the whole {nx}x{ny} raster per step"},
+                          "e2e": {"value": rate, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                          "gpu_launches": 0}), flush=True)
+        return
     cfg = make(args.config, nx=args.nx, ny=args.ny)
     crop = min(512, cfg.nx, cfg.ny)
     # warm-up then timed steps, each a single Heun step of the crop

@@ -184,6 +184,18 @@ int swof_ctx_launches_per_step(const swof_ctx* c);
  * device; mismatches[0..2] receive the bitwise mismatch counts (rcp, div, sqrt), all 0 when exact. */
 int swof_selftest_math(int64_t n, uint64_t seed, int64_t* mismatches);
 
+/* D8 flow direction of a DEM (the paper's user function): for every point
+ * of the ny x nx row-major raster z (x fastest, rows growing northwards), dir receives the code 1..8 of
+ * the lowest of its 8 neighbours that is > 0 and strictly below the point -- neighbours enumerated E,
+ * SE, S, SW, W, NW, N, NE (SPEC.md flow_direction), the first one on ties -- or 0 if there is none.
+ * Neighbours outside the raster are absent; values <= 0 (no-data) are never chosen.  z (fp64, or fp32
+ * for the _f32 entry point, the paper's DMatrix<float>) and dir (1 byte per point) may be host or device
+ * pointers; host buffers are staged through temporary device memory.  Work is enqueued on cuda_stream
+ * (NULL: legacy default stream); the call returns after it completed.  Returns SWOF_EINVAL for a NULL
+ * pointer or nx, ny < 1, SWOF_ENOMEM / SWOF_ECUDA on runtime failures.  Needs no context. */
+int swof_flow_direction(const double* z, int32_t nx, int32_t ny, uint8_t* dir, void* cuda_stream);
+int swof_flow_direction_f32(const float* z, int32_t nx, int32_t ny, uint8_t* dir, void* cuda_stream);
+
 void swof_destroy(swof_ctx* c);
 const char* swof_last_error(const swof_ctx* c);
 const char* swof_strerror(int code);

@@ -4,5 +4,5 @@
 The product path is libswof.so (csrc/, include/swof.h); this package never imports the oracle.
 """
 from .swof import (  # noqa: F401
-    EXPORTS, SwofDiag, SwofError, SwofParams, Solver, lib, params_from_config,
+    EXPORTS, SwofDiag, SwofError, SwofParams, Solver, flow_direction, lib, params_from_config,
 )

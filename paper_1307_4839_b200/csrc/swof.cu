@@ -15,6 +15,7 @@
 
 #include "../../include/swof.h"
 #include "swof_kernels.cuh"
+#include "swof_d8.cuh"
 
 using namespace swof;
 
@@ -537,6 +538,60 @@ int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms) {
     int rc;
     if ((rc = read_state(c))) return rc;
     return flags_rc(c);
+}
+
+}  // extern "C"
+
+namespace {
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+int flow_direction_impl(const T* z, int32_t nx, int32_t ny, uint8_t* dir, void* stream) {
+    if (!z || !dir || nx < 1 || ny < 1) return SWOF_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n = (size_t)nx * (size_t)ny;
+    const T* dz = z;
+    uint8_t* dd = dir;
+    T* tz = nullptr;
+    uint8_t* td = nullptr;
+    int rc = SWOF_OK;
+    if (!is_device_ptr(z)) {                             // host raster: stage it on the device
+        if (cudaMalloc(&tz, n * sizeof(T)) != cudaSuccess) return SWOF_ENOMEM;
+        if (cudaMemcpyAsync(tz, z, n * sizeof(T), cudaMemcpyHostToDevice, s) != cudaSuccess) rc = SWOF_ECUDA;
+        dz = tz;
+    }
+    if (!rc && !is_device_ptr(dir)) {
+        if (cudaMalloc(&td, n) != cudaSuccess) rc = SWOF_ENOMEM;
+        dd = td;
+    }
+    if (!rc) {
+        const dim3 grid((unsigned)((nx + D8_TX - 1) / D8_TX), (unsigned)((ny + D8Tile<T>::TY - 1) / D8Tile<T>::TY));
+        d8_kernel<T><<<grid, D8_NT, 0, s>>>(dz, nx, ny, dd);
+        if (cudaGetLastError() != cudaSuccess) rc = SWOF_ECUDA;
+    }
+    if (!rc && td && cudaMemcpyAsync(dir, td, n, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = SWOF_ECUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess && !rc) rc = SWOF_ECUDA;
+    if (tz) cudaFree(tz);
+    if (td) cudaFree(td);
+    return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int swof_flow_direction(const double* z, int32_t nx, int32_t ny, uint8_t* dir, void* cuda_stream) {
+    return flow_direction_impl<double>(z, nx, ny, dir, cuda_stream);
+}
+
+int swof_flow_direction_f32(const float* z, int32_t nx, int32_t ny, uint8_t* dir, void* cuda_stream) {
+    return flow_direction_impl<float>(z, nx, ny, dir, cuda_stream);
 }
 
 void swof_destroy(swof_ctx* c) {

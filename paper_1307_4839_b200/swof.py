@@ -25,7 +25,7 @@ FLAG_NONFINITE, FLAG_BIGCLAMP, FLAG_BADINPUT = 1, 2, 4
 EXPORTS = ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run", "swof_get_state",
            "swof_get_dt_history", "swof_get_diag", "swof_predictor", "swof_step_profiled",
            "swof_launches_per_step", "swof_ctx_launches_per_step", "swof_selftest_math", "swof_destroy",
-           "swof_last_error", "swof_strerror")
+           "swof_last_error", "swof_strerror", "swof_flow_direction", "swof_flow_direction_f32")
 
 
 class SwofParams(C.Structure):
@@ -88,6 +88,8 @@ def lib():
         L.swof_launches_per_step.argtypes = []
         L.swof_ctx_launches_per_step.argtypes = [vp]
         L.swof_selftest_math.argtypes = [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]
+        L.swof_flow_direction.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]
+        L.swof_flow_direction_f32.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]
         L.swof_destroy.argtypes = [vp]
         L.swof_destroy.restype = None
         L.swof_last_error.argtypes = [vp]
@@ -97,7 +99,7 @@ def lib():
         for name in ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run",
                      "swof_get_state", "swof_get_dt_history", "swof_get_diag", "swof_predictor",
                      "swof_step_profiled", "swof_launches_per_step", "swof_ctx_launches_per_step",
-                     "swof_selftest_math"):
+                     "swof_selftest_math", "swof_flow_direction", "swof_flow_direction_f32"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -260,3 +262,35 @@ def selftest_math(n: int = 1 << 24, seed: int = 1307):
     if rc != SWOF_OK:
         raise SwofError(rc, "selftest_math failed")
     return tuple(out)
+
+
+def flow_direction(z, out=None, stream=None):
+    """D8 flow direction (include/swof.h swof_flow_direction) of a (ny, nx) DEM: numpy or torch, host or
+    CUDA, float64 or float32.  Returns `out` (uint8 codes 0..8; allocated like z if None)."""
+    L = lib()
+    is_torch = hasattr(z, "data_ptr")
+    if is_torch:
+        import torch
+        assert z.is_contiguous() and z.dim() == 2 and z.dtype in (torch.float64, torch.float32)
+        ny, nx = z.shape
+        f32 = z.dtype == torch.float32
+        if out is None:
+            out = torch.empty((ny, nx), dtype=torch.uint8, device=z.device)
+        zp = C.c_void_p(z.data_ptr())
+        if stream is None and z.is_cuda:
+            stream = torch.cuda.current_stream(z.device)
+    else:
+        z = np.ascontiguousarray(z)
+        assert z.ndim == 2 and z.dtype in (np.float64, np.float32)
+        ny, nx = z.shape
+        f32 = z.dtype == np.float32
+        if out is None:
+            out = np.empty((ny, nx), dtype=np.uint8)
+        zp = C.c_void_p(z.ctypes.data)
+    op = C.c_void_p(out.data_ptr()) if hasattr(out, "data_ptr") else C.c_void_p(out.ctypes.data)
+    sp = C.c_void_p(stream.cuda_stream) if stream is not None else None
+    fn = L.swof_flow_direction_f32 if f32 else L.swof_flow_direction
+    rc = fn(zp, nx, ny, op, sp)
+    if rc != SWOF_OK:
+        raise SwofError(rc, L.swof_strerror(rc).decode())
+    return out

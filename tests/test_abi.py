@@ -20,7 +20,7 @@ def L():
 def declared_functions():
     text = (ROOT / "include" / "swof.h").read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(swof_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(swof_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declares_the_boundary():
