@@ -178,6 +178,9 @@ def main():
     ap.add_argument("--cpu-crop", type=int, default=1024)
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--workload", default="swof", choices=("swof", "d8"))
+    ap.add_argument("--shard", action="store_true",
+                    help="N > 1: split the one grid into row strips over the ranks (strong scaling, NCCL halo "
+                         "exchange + CFL all-reduce per step) instead of N independent replicas")
     ap.add_argument("--d8-dtype", default="f32", choices=("f32", "f64"))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -188,6 +191,8 @@ def main():
         return reference_arm(args, rank, world)
     if args.workload == "d8":
         return bench_d8(args, rank, world, local)
+    if args.shard:
+        return bench_shard(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -317,6 +322,55 @@ def main():
                            "peak_note": f"148 SMs x 64 fp64 lanes x {fmax_mhz:.0f} MHz (sm_max, {src})"}
     print(json.dumps(out), flush=True)
     solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_shard(args, rank, world, local):
+    """--shard: the workload's ONE grid cut into `world` row strips (the paper's MPI design,
+    P:731-760), one per rank/GPU; per step two NCCL halo exchanges of 2 rows x 3 fields with each
+    neighbour and one all-reduce(max) of the 2 CFL words.  Strong scaling: value = cells x steps / the
+    slowest rank's time."""
+    import torch
+    import torch.distributed as dist
+    from paper_1307_4839_b200.sharded import DistExchanger, ShardedSolver
+    from workloads import make
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    cfg = make(args.config, nx=args.nx, ny=args.ny)
+    cells = cfg.nx * cfg.ny
+    stream = torch.cuda.Stream()
+    s = ShardedSolver(cfg, world, [rank], DistExchanger(rank, world), stream=stream)
+    s.set_state(cfg.h, cfg.hu, cfg.hv, cfg.vinf if cfg.ga is not None else None, 0.0)
+    s.step(args.warmup)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        s.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = reduce_max(e0.elapsed_time(e1), world, "cuda")
+    st = s.get_state()
+    s.close()
+    if rank == 0:
+        out = {"metric": METRIC, "value": cells * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded cfg4 recipe, SURVEY.md §8d)",
+               "config": {"workload": args.config, "nx": cfg.nx, "ny": cfg.ny, "cells": cells,
+                          "parallelism": f"row strips x{world} (NCCL halo exchange + CFL all-reduce)",
+                          "l2": "inputs larger than L2; no flush"},
+               "gpu_launches": args.steps * (2 + (cfg.cfl_mode == "face")), "clocks": clk.summary(),
+               "t": st["t"], "step": st["step"]}
+        print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -51,6 +51,9 @@ extern "C" {
 #define SWOF_BC_FREE 1      /* zero-gradient copy of interior layer 0 (h, q, z)                  */
 #define SWOF_BC_PERIODIC 2  /* wrap (both opposite sides must be PERIODIC)                      */
 #define SWOF_BC_INFLOW 3    /* imposed (h_c(q), q = Q(t)/W, 0) on [k0, k1), WALL elsewhere        */
+#define SWOF_BC_HALO 4      /* S/N only: the side borders another row strip of a decomposed grid
+                               (the paper's MPI strips): its 2 ghost rows
+                               are filled by the caller's halo exchange, see swof_halo_rows        */
 
 /* scheme variants; zero-initialised params give the paper's recommended
  * scheme: HLL, second order (MUSCL + Heun), CFL on cell-centred speeds, Green-Ampt as printed */
@@ -105,6 +108,9 @@ typedef struct swof_params {
                                 space (no reconstruction) and explicit Euler in time      */
     int32_t cfl_mode;        /* SWOF_CFL_*                                                        */
     int32_t ga_form;         /* SWOF_GA_*                                                         */
+    double inflow_width[4];  /* width W [m] that Q(t) is spread over per side (0: the segment's own
+                                (k1 - k0) * dy or dx); a strip of a decomposed grid passes the global
+                                segment's width and its share of Q so that q = Q/W is unchanged   */
 } swof_params;
 
 typedef struct swof_diag {
@@ -183,6 +189,36 @@ int swof_ctx_launches_per_step(const swof_ctx* c);
  * library operators on n random operands (exponents in [-60, 60], sqrt in [-80, 40]) on the current
  * device; mismatches[0..2] receive the bitwise mismatch counts (rcp, div, sqrt), all 0 when exact. */
 int swof_selftest_math(int64_t n, uint64_t seed, int64_t* mismatches);
+
+/* ---- row-strip decomposition (PAPER.md P:731-760 on NVLink) ----
+ * A strip is an ordinary context whose S and/or N side is SWOF_BC_HALO.  The caller (one rank per GPU,
+ * or several strips driven from one process) runs each time step as
+ *   phase 0 (predictor) -> exchange set 1 -> phase 1 (corrector / order-1 commit) -> exchange set 0
+ *   -> phase 2 (face CFL, if any) -> all-reduce (max) of the 2 words at swof_cfl_maxima
+ * and, once after swof_create, exchanges set 2 (z); after swof_set_state it exchanges set 0, calls
+ * swof_refresh_cfl and all-reduces.  Every strip then computes exactly what the undivided grid
+ * computes on its rows (bit for bit: the ghost rows carry the neighbours' values).
+ *
+ * swof_halo_rows: device pointers of the 2 boundary rows this strip sends to its neighbour on `side`
+ *   (SWOF_SIDE_S or SWOF_SIDE_N) and of the 2 ghost rows it receives from it, for field set `set`:
+ *   0 = the state U^n (h, hu, hv), read by the predictor; 1 = the predictor's output U* (h, hu, hv),
+ *   read by the corrector; 2 = the topography z (send[0]/recv[0] only, the others NULL).  Each block is
+ *   2 rows x pitch doubles, contiguous (*bytes).  The S block of a strip goes to the N ghost rows of
+ *   the strip below and vice versa.
+ * swof_enqueue_phase: enqueue phase 0, 1 or 2 of the next time step on the context's stream and return
+ *   without synchronising (phase 2 is a no-op unless SWOF_CFL_FACE; it ends the step).
+ * swof_cfl_maxima: device pointer to the 2 uint64 words (a_x, a_y as IEEE bit patterns; max-reduce them
+ *   as unsigned or as int64) that the next step's kernels derive dt from.
+ * swof_refresh_cfl: recompute those maxima from the current state (cell or face form, local rows).
+ * swof_set_limits: t_end and the absolute step limit of the following phases (steps past them are
+ *   exact no-ops); swof_step / swof_run set their own.
+ * swof_sync: wait for the context's stream; returns SWOF_ENUMERIC if a flag is set. */
+int swof_halo_rows(swof_ctx* c, int32_t set, int32_t side, double** send, double** recv, size_t* bytes);
+int swof_enqueue_phase(swof_ctx* c, int32_t phase);
+int swof_cfl_maxima(swof_ctx* c, uint64_t** dev_ptr);
+int swof_refresh_cfl(swof_ctx* c);
+int swof_set_limits(swof_ctx* c, double t_end, int64_t step_limit);
+int swof_sync(swof_ctx* c);
 
 /* D8 flow direction of a DEM (the paper's user function): for every point
  * of the ny x nx row-major raster z (x fastest, rows growing northwards), dir receives the code 1..8 of

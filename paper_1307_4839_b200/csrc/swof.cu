@@ -54,7 +54,9 @@ struct Layout {
 Layout make_layout(const swof_params* p, bool fric_field) {
     Layout L{};
     L.pitch = align_up((size_t)p->nx, 32);
-    L.field = align_up(L.pitch * sizeof(double) * (size_t)p->ny, 256);
+    // every field carries GHOST_ROWS spare rows below and above (the halo rows of a strip's HALO sides);
+    // the field pointers address row 0, which stays 256-B aligned
+    L.field = align_up(L.pitch * sizeof(double) * ((size_t)p->ny + 2 * GHOST_ROWS), 256);
     size_t o = 0;
     L.off_A = o; o += 3 * L.field;
     L.off_B = o; o += 3 * L.field;
@@ -90,7 +92,10 @@ const char* validate(const swof_params* p) {
         if (k > 0 && !(p->rain_t[k] > p->rain_t[k - 1])) return "rain_t must be ascending";
     }
     for (int s = 0; s < 4; ++s) {
-        if (p->bc[s] < SWOF_BC_WALL || p->bc[s] > SWOF_BC_INFLOW) return "unknown boundary type";
+        if (p->bc[s] < SWOF_BC_WALL || p->bc[s] > SWOF_BC_HALO) return "unknown boundary type";
+        if (p->bc[s] == SWOF_BC_HALO && s < 2) return "HALO (strip) sides are S and N only";
+        if (p->bc[s] == SWOF_BC_HALO && p->ny < 2) return "a strip needs >= 2 rows";
+        if (!(p->inflow_width[s] >= 0) || !std::isfinite(p->inflow_width[s])) return "inflow_width must be finite and >= 0";
         const int n = (s < 2) ? p->ny : p->nx;
         if (p->bc[s] == SWOF_BC_INFLOW) {
             if (p->inflow_k0[s] < 0 || p->inflow_k1[s] > n || p->inflow_k0[s] >= p->inflow_k1[s])
@@ -281,12 +286,13 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     char* base = (char*)c->ws;
     KBufs& b = c->kb;
     const size_t F = L.field;
-    b.Ah = (double*)(base + L.off_A); b.Ahu = (double*)(base + L.off_A + F); b.Ahv = (double*)(base + L.off_A + 2 * F);
-    b.Bh = (double*)(base + L.off_B); b.Bhu = (double*)(base + L.off_B + F); b.Bhv = (double*)(base + L.off_B + 2 * F);
-    b.z = (double*)(base + L.off_z);
-    b.VA = p->ga_enabled ? (double*)(base + L.off_VA) : nullptr;
-    b.VB = p->ga_enabled ? (double*)(base + L.off_VB) : nullptr;
-    b.fric = has_ff ? (double*)(base + L.off_fric) : nullptr;
+    const size_t g = (size_t)GHOST_ROWS * L.pitch * sizeof(double);      // row 0 of a field
+    b.Ah = (double*)(base + L.off_A + g); b.Ahu = (double*)(base + L.off_A + F + g); b.Ahv = (double*)(base + L.off_A + 2 * F + g);
+    b.Bh = (double*)(base + L.off_B + g); b.Bhu = (double*)(base + L.off_B + F + g); b.Bhv = (double*)(base + L.off_B + 2 * F + g);
+    b.z = (double*)(base + L.off_z + g);
+    b.VA = p->ga_enabled ? (double*)(base + L.off_VA + g) : nullptr;
+    b.VB = p->ga_enabled ? (double*)(base + L.off_VB + g) : nullptr;
+    b.fric = has_ff ? (double*)(base + L.off_fric + g) : nullptr;
     b.st = (DevState*)(base + L.off_st);
     b.dt_hist = (double*)(base + L.off_hist);
     b.dt_cap = p->dt_hist_cap > 0 ? p->dt_hist_cap : (int64_t)1 << 20;
@@ -312,7 +318,8 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
         k.bc[s] = p->bc[s];
         k.k0[s] = p->inflow_k0[s]; k.k1[s] = p->inflow_k1[s];
         k.n_hydro[s] = p->bc[s] == SWOF_BC_INFLOW ? p->n_hydro[s] : 0;
-        k.width[s] = (double)(p->inflow_k1[s] - p->inflow_k0[s]) * ((s < 2) ? p->dy : p->dx);
+        k.width[s] = p->inflow_width[s] > 0 ? p->inflow_width[s]
+                   : (double)(p->inflow_k1[s] - p->inflow_k0[s]) * ((s < 2) ? p->dy : p->dx);
         for (int i = 0; i < k.n_hydro[s]; ++i) { k.hydro_t[s][i] = p->hydro_t[s][i]; k.hydro_q[s][i] = p->hydro_q[s][i]; }
     }
     c->grid = dim3((unsigned)((p->nx + TX - 1) / TX), (unsigned)((p->ny + TY - 1) / TY));
@@ -535,6 +542,80 @@ int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms) {
     for (auto& e : ev) cudaEventDestroy(e);
     ms[0] = acc[0];
     ms[1] = acc[1];
+    int rc;
+    if ((rc = read_state(c))) return rc;
+    return flags_rc(c);
+}
+
+int swof_halo_rows(swof_ctx* c, int32_t set, int32_t side, double** send, double** recv, size_t* bytes) {
+    if (!c || !send || !recv || (side != SWOF_SIDE_S && side != SWOF_SIDE_N) || set < 0 || set > 2)
+        return SWOF_EINVAL;
+    const size_t pitch = (size_t)c->kp.pitch, ny = (size_t)c->p.ny;
+    double* f[3] = {nullptr, nullptr, nullptr};
+    if (set == 0) { f[0] = c->kb.Ah; f[1] = c->kb.Ahu; f[2] = c->kb.Ahv; }
+    else if (set == 1) { f[0] = c->kb.Bh; f[1] = c->kb.Bhu; f[2] = c->kb.Bhv; }
+    else f[0] = c->kb.z;
+    for (int k = 0; k < 3; ++k) {
+        send[k] = recv[k] = nullptr;
+        if (!f[k]) continue;
+        if (side == SWOF_SIDE_S) {            // rows 0, 1 go south; rows -2, -1 come from the south
+            send[k] = f[k];
+            recv[k] = f[k] - GHOST_ROWS * pitch;
+        } else {                              // rows ny-2, ny-1 go north; rows ny, ny+1 come from it
+            send[k] = f[k] + (ny - GHOST_ROWS) * pitch;
+            recv[k] = f[k] + ny * pitch;
+        }
+    }
+    if (bytes) *bytes = GHOST_ROWS * pitch * sizeof(double);
+    return SWOF_OK;
+}
+
+int swof_enqueue_phase(swof_ctx* c, int32_t phase) {
+    if (!c) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_enqueue_phase before swof_set_state");
+    if (phase == 0) {
+        c->kpred<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+    } else if (phase == 1) {
+        if (c->kp.order == 1) euler_commit_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, c->par);
+        else c->kcorr<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+    } else if (phase == 2) {
+        if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, c->par, 0);
+        c->par ^= 1;                          // the step is complete
+    } else {
+        return fail(c, SWOF_EINVAL, "phase must be 0, 1 or 2");
+    }
+    CK(cudaGetLastError());
+    return SWOF_OK;
+}
+
+int swof_cfl_maxima(swof_ctx* c, uint64_t** dev_ptr) {
+    if (!c || !dev_ptr) return SWOF_EINVAL;
+    *dev_ptr = (uint64_t*)&c->kb.st->amax[c->par][0];
+    return SWOF_OK;
+}
+
+int swof_refresh_cfl(swof_ctx* c) {
+    if (!c) return SWOF_EINVAL;
+    if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_refresh_cfl before swof_set_state");
+    if (c->par != 0) return fail(c, SWOF_ESTATE, "swof_refresh_cfl only right after swof_set_state");
+    CK(cudaMemsetAsync(&c->kb.st->amax[0][0], 0, 2 * sizeof(unsigned long long), c->stream));
+    if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, 0, 1);
+    else init_cfl_kernel<<<1184, 256, 0, c->stream>>>(c->kp, c->kb);
+    CK(cudaGetLastError());
+    return SWOF_OK;
+}
+
+int swof_set_limits(swof_ctx* c, double t_end, int64_t step_limit) {
+    if (!c || std::isnan(t_end)) return SWOF_EINVAL;
+    const long long lim = (long long)step_limit;
+    CK(cudaMemcpyAsync(&c->kb.st->t_end, &t_end, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(&c->kb.st->step_limit, &lim, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));      // the host values are stack temporaries
+    return SWOF_OK;
+}
+
+int swof_sync(swof_ctx* c) {
+    if (!c) return SWOF_EINVAL;
     int rc;
     if ((rc = read_state(c))) return rc;
     return flags_rc(c);

@@ -15,7 +15,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "libswof.so"
 
 SWOF_OK, SWOF_EINVAL, SWOF_ENUMERIC, SWOF_ECUDA, SWOF_ENOMEM, SWOF_ESTATE = range(6)
 FRIC = {"none": 0, "manning": 1, "strickler": 2, "darcy_weisbach": 3, "chezy": 4}
-BC = {"wall": 0, "free": 1, "periodic": 2, "inflow": 3}
+BC = {"wall": 0, "free": 1, "periodic": 2, "inflow": 3, "halo": 4}
 FLUX = {"hll": 0, "rusanov": 1}
 CFL_MODE = {"cell": 0, "face": 1}
 GA_FORM = {"printed": 0, "darcy": 1}
@@ -25,7 +25,10 @@ FLAG_NONFINITE, FLAG_BIGCLAMP, FLAG_BADINPUT = 1, 2, 4
 EXPORTS = ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run", "swof_get_state",
            "swof_get_dt_history", "swof_get_diag", "swof_predictor", "swof_step_profiled",
            "swof_launches_per_step", "swof_ctx_launches_per_step", "swof_selftest_math", "swof_destroy",
-           "swof_last_error", "swof_strerror", "swof_flow_direction", "swof_flow_direction_f32")
+           "swof_last_error", "swof_strerror", "swof_flow_direction", "swof_flow_direction_f32",
+           "swof_halo_rows", "swof_enqueue_phase", "swof_cfl_maxima", "swof_refresh_cfl", "swof_set_limits",
+           "swof_sync")
+SIDE_S, SIDE_N = 2, 3
 
 
 class SwofParams(C.Structure):
@@ -41,6 +44,7 @@ class SwofParams(C.Structure):
         ("n_hydro", C.c_int32 * 4), ("hydro_t", (C.c_double * MAXT) * 4), ("hydro_q", (C.c_double * MAXT) * 4),
         ("dt_hist_cap", C.c_int64), ("graph_steps", C.c_int32), ("clamp_fail", C.c_double),
         ("flux", C.c_int32), ("order", C.c_int32), ("cfl_mode", C.c_int32), ("ga_form", C.c_int32),
+        ("inflow_width", C.c_double * 4),
     ]
 
 
@@ -90,6 +94,13 @@ def lib():
         L.swof_selftest_math.argtypes = [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]
         L.swof_flow_direction.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]
         L.swof_flow_direction_f32.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]
+        PD = C.POINTER(C.c_void_p)
+        L.swof_halo_rows.argtypes = [vp, C.c_int32, C.c_int32, PD, PD, C.POINTER(C.c_size_t)]
+        L.swof_enqueue_phase.argtypes = [vp, C.c_int32]
+        L.swof_cfl_maxima.argtypes = [vp, PD]
+        L.swof_refresh_cfl.argtypes = [vp]
+        L.swof_set_limits.argtypes = [vp, C.c_double, C.c_int64]
+        L.swof_sync.argtypes = [vp]
         L.swof_destroy.argtypes = [vp]
         L.swof_destroy.restype = None
         L.swof_last_error.argtypes = [vp]
@@ -99,7 +110,8 @@ def lib():
         for name in ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", "swof_run",
                      "swof_get_state", "swof_get_dt_history", "swof_get_diag", "swof_predictor",
                      "swof_step_profiled", "swof_launches_per_step", "swof_ctx_launches_per_step",
-                     "swof_selftest_math", "swof_flow_direction", "swof_flow_direction_f32"):
+                     "swof_selftest_math", "swof_flow_direction", "swof_flow_direction_f32", "swof_halo_rows",
+                     "swof_enqueue_phase", "swof_cfl_maxima", "swof_refresh_cfl", "swof_set_limits", "swof_sync"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -125,6 +137,7 @@ def params_from_config(cfg, graph_steps: int = 0, dt_hist_cap: int = 0) -> SwofP
             p.n_hydro[s] = len(fl.hydro_t)
             for k, (t, q) in enumerate(zip(fl.hydro_t, fl.hydro_q)):
                 p.hydro_t[s][k], p.hydro_q[s][k] = t, q
+            p.inflow_width[s] = float(getattr(fl, "width", 0.0) or 0.0)
     p.dt_hist_cap = dt_hist_cap
     p.graph_steps = graph_steps
     p.flux = FLUX[getattr(cfg, "flux", "hll")]
@@ -249,6 +262,43 @@ class Solver:
         ms = (C.c_double * 2)()
         self._check(self._L.swof_step_profiled(self._ctx, int(nsteps), ms))
         return ms[0], ms[1]
+
+    # -- row-strip decomposition support (include/swof.h, SWOF_BC_HALO)
+    def _view(self, ptr: int, nbytes: int, dtype):
+        """torch view of `nbytes` of this context's workspace starting at device address `ptr`."""
+        assert self._ws is not None, "strip views need the torch workspace"
+        off = ptr - self._ws.data_ptr()
+        assert 0 <= off and off + nbytes <= self._ws.numel()
+        return self._ws[off: off + nbytes].view(dtype)
+
+    def halo_rows(self, field_set: int, side: int):
+        """([send views], [recv views]) of the 2-row blocks of field set 0 (U^n), 1 (U*) or 2 (z)."""
+        import torch
+        send, recv = (C.c_void_p * 3)(), (C.c_void_p * 3)()
+        nb = C.c_size_t()
+        self._check(self._L.swof_halo_rows(self._ctx, field_set, side, send, recv, C.byref(nb)))
+        sv = [self._view(send[k], nb.value, torch.float64) for k in range(3) if send[k]]
+        rv = [self._view(recv[k], nb.value, torch.float64) for k in range(3) if recv[k]]
+        return sv, rv
+
+    def enqueue_phase(self, phase: int):
+        self._check(self._L.swof_enqueue_phase(self._ctx, phase))
+
+    def cfl_maxima(self):
+        """int64 view of the 2 CFL maxima words the next step reads (max-reduce them across strips)."""
+        import torch
+        ptr = C.c_void_p()
+        self._check(self._L.swof_cfl_maxima(self._ctx, C.byref(ptr)))
+        return self._view(ptr.value, 16, torch.int64)
+
+    def refresh_cfl(self):
+        self._check(self._L.swof_refresh_cfl(self._ctx))
+
+    def set_limits(self, t_end: float = float("inf"), step_limit: int = (1 << 63) - 1):
+        self._check(self._L.swof_set_limits(self._ctx, float(t_end), int(step_limit)))
+
+    def sync(self):
+        self._check(self._L.swof_sync(self._ctx))
 
     def launches_per_step(self) -> int:
         """Kernel launches one time step of this context issues."""

@@ -42,6 +42,8 @@ class Inflow:
     k1: int                      # one past the last
     hydro_t: list                # hydrograph times [s] (piecewise linear, clamped at the ends)
     hydro_q: list                # discharge Q(t) [m^3/s] over the whole segment
+    width: float = 0.0           # width Q is spread over [m] (0: the segment's own); strips of a
+                                 # decomposed grid keep the global segment's width (paper_1307_4839_b200.sharded)
 
 
 @dataclass
