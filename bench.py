@@ -310,7 +310,8 @@ def main():
             with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
                 prof = json.load(f)
             for kname, k in prof["kernels"].items():
-                if ("<1>" in kname) == (dom == "corrector"):
+                is_corr = "stage_kernel<(bool)1" in kname or "stage_kernel<1>" in kname or "<true" in kname
+                if is_corr == (dom == "corrector"):
                     traffic = k["dram_bytes_per_cell"] * cells
                     tsrc = f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"
         except Exception:
