@@ -29,7 +29,10 @@ __global__ void __launch_bounds__(D8_NT) d8_kernel(const T* __restrict__ z, int 
     __shared__ T s[D8_LH][D8_LW];
     const int i0 = blockIdx.x * D8_TX, j0 = blockIdx.y * D8_TY;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const T absent = T(-1);                                          // fails "> 0": never chosen
+    // shared memory holds t = (v > 0) ? v : NaN: the listing's test "n > 0 && n < min" becomes "t < min"
+    // (a NaN compares false), and the centre's own start value min = t_centre behaves exactly like the
+    // raw value (a centre <= 0 or NaN admits no neighbour either way); absent neighbours are NaN too
+    const T nan = __int_as_float(0x7fc00000) * T(1);
     // stage the tile + 1-point halo: warp w loads rows w, w + 8, ...; lanes walk the row
     for (int r = warp; r < D8_LH; r += D8_NT / 32) {
         const int gj = j0 + r - 1;
@@ -39,7 +42,8 @@ __global__ void __launch_bounds__(D8_NT) d8_kernel(const T* __restrict__ z, int 
 #pragma unroll
         for (int k = 0; k < (D8_LW + 31) / 32; ++k) {
             const int c = lane + 32 * k, gi = i0 + c - 1;
-            v[k] = (rowok && c < D8_LW && gi >= 0 && gi < nx) ? row[gi] : absent;
+            const T x = (rowok && c < D8_LW && gi >= 0 && gi < nx) ? row[gi] : nan;
+            v[k] = x > T(0) ? x : nan;
         }
 #pragma unroll
         for (int k = 0; k < (D8_LW + 31) / 32; ++k) {
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(D8_NT) d8_kernel(const T* __restrict__ z, int 
         int index = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            if (nb[k] > T(0) && nb[k] < mn) {
+            if (nb[k] < mn) {
                 index = k + 1;
                 mn = nb[k];
             }
