@@ -214,6 +214,23 @@ int swof_selftest_math(int64_t n, uint64_t seed, int64_t* mismatches);
  *   exact no-ops); swof_step / swof_run set their own.
  * swof_sync: wait for the context's stream; returns SWOF_ENUMERIC if a flag is set. */
 int swof_halo_rows(swof_ctx* c, int32_t set, int32_t side, double** send, double** recv, size_t* bytes);
+/* Fused halo exchange: the kernels that produce U* (set 1) and U^{n+1} (set 0) also store this strip's 2
+ * boundary rows on `side` straight into the neighbour's ghost rows -- set0[k], set1[k] (k = h, hu, hv) are
+ * the neighbour's receive blocks for this side (its swof_halo_rows(set, opposite side) recv pointers, in
+ * this process's address space: same device, or NVLink peer memory mapped with CUDA IPC).  The caller
+ * then replaces the per-phase exchanges of sets 0 and 1 by a barrier between strips (the state loaded by
+ * swof_set_state still needs one ordinary exchange).  NULL arrays disable it. */
+int swof_set_halo_push(swof_ctx* c, int32_t side, double* const* set0, double* const* set1);
+/* CUDA IPC for strips in different processes: swof_ipc_handle writes the 64-byte cudaIpcMemHandle_t of
+ * the context's workspace (library-allocated only: d_workspace == NULL at create) and its base address
+ * in the owner's address space (subtract it from swof_halo_rows pointers to get offsets); swof_ipc_open
+ * maps a neighbour's workspace into this process (peer access enabled lazily), swof_ipc_close unmaps. */
+int swof_ipc_handle(swof_ctx* c, void* handle, uint64_t* ws_base);
+int swof_ipc_open(const void* handle, void** base);
+int swof_ipc_close(void* base);
+/* Enqueue a copy of `bytes` between any two addresses (host, device, mapped peer) on cuda_stream; used
+ * by the strip driver to pull a neighbour's rows out of its mapped workspace. */
+int swof_copy(void* dst, const void* src, size_t bytes, void* cuda_stream);
 int swof_enqueue_phase(swof_ctx* c, int32_t phase);
 int swof_cfl_maxima(swof_ctx* c, uint64_t** dev_ptr);
 int swof_refresh_cfl(swof_ctx* c);

@@ -294,6 +294,7 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     b.VB = p->ga_enabled ? (double*)(base + L.off_VB + g) : nullptr;
     b.fric = has_ff ? (double*)(base + L.off_fric + g) : nullptr;
     b.st = (DevState*)(base + L.off_st);
+    std::memset(b.push, 0, sizeof(b.push));
     b.dt_hist = (double*)(base + L.off_hist);
     b.dt_cap = p->dt_hist_cap > 0 ? p->dt_hist_cap : (int64_t)1 << 20;
     c->d_part = (double*)(base + L.off_part);
@@ -568,6 +569,48 @@ int swof_halo_rows(swof_ctx* c, int32_t set, int32_t side, double** send, double
     }
     if (bytes) *bytes = GHOST_ROWS * pitch * sizeof(double);
     return SWOF_OK;
+}
+
+int swof_set_halo_push(swof_ctx* c, int32_t side, double* const* set0, double* const* set1) {
+    if (!c || (side != SWOF_SIDE_S && side != SWOF_SIDE_N)) return SWOF_EINVAL;
+    if (c->p.bc[side] != SWOF_BC_HALO) return fail(c, SWOF_EINVAL, "halo push needs a SWOF_BC_HALO side");
+    const int s = side == SWOF_SIDE_S ? 0 : 1;
+    for (int k = 0; k < 3; ++k) {
+        c->kb.push[s][0][k] = set0 ? set0[k] : nullptr;
+        c->kb.push[s][1][k] = set1 ? set1[k] : nullptr;
+    }
+    if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }   // kernel params changed
+    return SWOF_OK;
+}
+
+int swof_ipc_handle(swof_ctx* c, void* handle, uint64_t* ws_base) {
+    if (!c || !handle) return SWOF_EINVAL;
+    if (!c->own_ws) return fail(c, SWOF_EINVAL, "IPC export needs the library-allocated workspace");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->ws));
+    std::memcpy(handle, &h, sizeof(h));
+    if (ws_base) *ws_base = (uint64_t)(uintptr_t)c->ws;
+    return SWOF_OK;
+}
+
+int swof_ipc_open(const void* handle, void** base) {
+    if (!handle || !base) return SWOF_EINVAL;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    if (cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { cudaGetLastError(); return SWOF_ECUDA; }
+    return SWOF_OK;
+}
+
+int swof_ipc_close(void* base) {
+    if (!base) return SWOF_EINVAL;
+    return cudaIpcCloseMemHandle(base) == cudaSuccess ? SWOF_OK : SWOF_ECUDA;
+}
+
+int swof_copy(void* dst, const void* src, size_t bytes, void* cuda_stream) {
+    if ((!dst || !src) && bytes) return SWOF_EINVAL;
+    if (!bytes) return SWOF_OK;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)cuda_stream) == cudaSuccess ? SWOF_OK
+                                                                                                      : SWOF_ECUDA;
 }
 
 int swof_enqueue_phase(swof_ctx* c, int32_t phase) {

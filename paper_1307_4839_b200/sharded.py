@@ -18,7 +18,7 @@ import copy
 
 import numpy as np
 
-from .swof import SIDE_N, SIDE_S, Solver, params_from_config
+from .swof import SIDE_N, SIDE_S, Solver, copy as dev_copy, ipc_close, ipc_open, params_from_config
 
 
 def strip_rows(ny: int, nranks: int, rank: int):
@@ -63,7 +63,16 @@ def strip_config(cfg, rank: int, nranks: int):
 
 class LocalExchanger:
     """All strips in this process (one stream): halo rows are device-to-device copies, the CFL all-reduce
-    a max over the strips' words."""
+    a max over the strips' words.  Fused mode: the kernels push their boundary rows into the neighbours'
+    ghost rows themselves (swof_set_halo_push) and stream order is the barrier."""
+
+    def link_push(self, strips):
+        for lo, hi in zip(strips[:-1], strips[1:]):
+            lo.set_halo_push(SIDE_N, hi.halo_block_addrs(0, SIDE_S)[1], hi.halo_block_addrs(1, SIDE_S)[1])
+            hi.set_halo_push(SIDE_S, lo.halo_block_addrs(0, SIDE_N)[1], lo.halo_block_addrs(1, SIDE_N)[1])
+
+    def barrier(self, strips):
+        pass
 
     def exchange(self, strips, field_set: int):
         for lo, hi in zip(strips[:-1], strips[1:]):
@@ -73,6 +82,9 @@ class LocalExchanger:
                 a.copy_(b)
             for a, b in zip(hi_recv, lo_send):
                 a.copy_(b)
+
+    def allreduce_max_strips(self, strips):
+        self.allreduce_max([sv.cfl_maxima() for sv in strips])
 
     def allreduce_max(self, words):
         import torch
@@ -107,6 +119,9 @@ class DistExchanger:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
 
+    def allreduce_max_strips(self, strips):
+        self.allreduce_max([sv.cfl_maxima() for sv in strips])
+
     def allreduce_max(self, words):
         import torch.distributed as dist
         (w,) = words
@@ -114,17 +129,100 @@ class DistExchanger:
             dist.all_reduce(w, op=dist.ReduceOp.MAX, group=self.group)
 
 
+class IpcExchanger:
+    """One strip per process, the neighbours' workspaces mapped with CUDA IPC (NVLink peer memory across
+    GPUs; also valid between processes sharing one GPU).  Fused mode only: the kernels push boundary rows
+    into the mapped neighbours; the state loaded by set_state is pulled once by copies.  Ordering between
+    strips is a host barrier after each phase (torch.distributed, any backend) and the CFL all-reduce is
+    host-staged -- correct by construction; an in-stream NCCL barrier is the faster production variant."""
+
+    def __init__(self, rank: int, nranks: int, group=None):
+        self.rank, self.nranks, self.group = rank, nranks, group
+        self.peers = {}                       # side -> (mapped base, info dict of the neighbour)
+
+    def _neighbours(self):
+        out = {}
+        if self.rank > 0:
+            out[SIDE_S] = self.rank - 1
+        if self.rank < self.nranks - 1:
+            out[SIDE_N] = self.rank + 1
+        return out
+
+    def link_push(self, strips):
+        import torch.distributed as dist
+        (sv,) = strips
+        handle, base = sv.ipc_handle()
+        info = {"handle": handle, "base": base, "blocks": {}}
+        for side in (SIDE_S, SIDE_N):
+            for fs in (0, 1, 2):
+                send, recv, nb = sv.halo_block_addrs(fs, side)
+                info["blocks"][(fs, side)] = ([a - base if a else 0 for a in send], [a - base if a else 0 for a in recv], nb)
+        allinfo = [None] * self.nranks
+        dist.all_gather_object(allinfo, info, group=self.group)
+        opposite = {SIDE_S: SIDE_N, SIDE_N: SIDE_S}
+        for side, nbr in self._neighbours().items():
+            other = allinfo[nbr]
+            mbase = ipc_open(other["handle"])
+            self.peers[side] = (mbase, other)
+            recv = [[mbase + off for off in other["blocks"][(fs, opposite[side])][1]] for fs in (0, 1)]
+            sv.set_halo_push(side, recv[0], recv[1])
+        self.barrier(strips)
+
+    def exchange(self, strips, field_set: int):
+        """Pull the neighbours' boundary rows of `field_set` into this strip's ghost rows (after a barrier)."""
+        (sv,) = strips
+        self.barrier(strips)
+        opposite = {SIDE_S: SIDE_N, SIDE_N: SIDE_S}
+        for side, (mbase, other) in self.peers.items():
+            _, recv, nb = sv.halo_block_addrs(field_set, side)
+            send_off, _, _ = other["blocks"][(field_set, opposite[side])]
+            for dst, off in zip(recv, send_off):
+                if dst and off:
+                    dev_copy(dst, mbase + off, nb, sv.stream)
+        self.barrier(strips)
+
+    def barrier(self, strips):
+        import torch.distributed as dist
+        for sv in strips:
+            sv.stream.synchronize()
+        dist.barrier(group=self.group)
+
+    def allreduce_max_strips(self, strips):
+        import torch
+        import torch.distributed as dist
+        (sv,) = strips
+        if self.nranks == 1:
+            return
+        addr = sv.cfl_maxima_addr()
+        host = torch.zeros(2, dtype=torch.int64)
+        dev_copy(host.data_ptr(), addr, 16, sv.stream)
+        sv.stream.synchronize()
+        dist.all_reduce(host, op=dist.ReduceOp.MAX, group=self.group)
+        dev_copy(addr, host.data_ptr(), 16, sv.stream)
+        sv.stream.synchronize()
+
+    def close(self):
+        for mbase, _ in self.peers.values():
+            ipc_close(mbase)
+        self.peers = {}
+
+
 class ShardedSolver:
     """The time step of `cfg` on row strips.  `ranks`: the strips this process drives (all of them with a
     LocalExchanger; its own rank with a DistExchanger)."""
 
-    def __init__(self, cfg, nranks: int, ranks, exchanger, stream=None, graph_steps: int = 0):
+    def __init__(self, cfg, nranks: int, ranks, exchanger, stream=None, graph_steps: int = 0, fused: bool = False):
+        """fused: the stage kernels push their boundary rows into the neighbours' ghost rows themselves
+        (no exchange pass; a barrier between phases); needs LocalExchanger or IpcExchanger."""
         import torch
-        self.cfg, self.nranks, self.ranks, self.ex = cfg, nranks, list(ranks), exchanger
+        self.cfg, self.nranks, self.ranks, self.ex, self.fused = cfg, nranks, list(ranks), exchanger, fused
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self.parts = [strip_config(cfg, r, nranks) for r in self.ranks]
-        self.strips = [Solver(params_from_config(p, graph_steps=graph_steps), p.z, p.fric_field, stream=self.stream)
-                       for p in self.parts]
+        ipc = isinstance(exchanger, IpcExchanger)
+        self.strips = [Solver(params_from_config(p, graph_steps=graph_steps), p.z, p.fric_field, stream=self.stream,
+                              use_torch_workspace=not ipc) for p in self.parts]
+        if fused or ipc:
+            self.ex.link_push(self.strips)
         with torch.cuda.stream(self.stream):
             self.ex.exchange(self.strips, 2)                 # z ghost rows, once
 
@@ -140,7 +238,7 @@ class ShardedSolver:
             self.ex.exchange(self.strips, 0)
             for sv in self.strips:
                 sv.refresh_cfl()
-            self.ex.allreduce_max([sv.cfl_maxima() for sv in self.strips])
+            self.ex.allreduce_max_strips(self.strips)
         for sv in self.strips:
             sv.sync()
 
@@ -152,13 +250,19 @@ class ShardedSolver:
             for _ in range(nsteps):
                 for sv in self.strips:
                     sv.enqueue_phase(0)
-                self.ex.exchange(self.strips, 1)
+                if self.fused:
+                    self.ex.barrier(self.strips)             # U* rows already pushed by the predictor
+                else:
+                    self.ex.exchange(self.strips, 1)
                 for sv in self.strips:
                     sv.enqueue_phase(1)
-                self.ex.exchange(self.strips, 0)
+                if self.fused:
+                    self.ex.barrier(self.strips)
+                else:
+                    self.ex.exchange(self.strips, 0)
                 for sv in self.strips:
                     sv.enqueue_phase(2)
-                self.ex.allreduce_max([sv.cfl_maxima() for sv in self.strips])
+                self.ex.allreduce_max_strips(self.strips)
         for sv in self.strips:
             sv.sync()
 
@@ -175,5 +279,7 @@ class ShardedSolver:
         return self.strips[0].dt_history()
 
     def close(self):
+        if hasattr(self.ex, "close"):
+            self.ex.close()
         for sv in self.strips:
             sv.close()

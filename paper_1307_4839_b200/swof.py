@@ -27,7 +27,8 @@ EXPORTS = ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", 
            "swof_launches_per_step", "swof_ctx_launches_per_step", "swof_selftest_math", "swof_destroy",
            "swof_last_error", "swof_strerror", "swof_flow_direction", "swof_flow_direction_f32",
            "swof_halo_rows", "swof_enqueue_phase", "swof_cfl_maxima", "swof_refresh_cfl", "swof_set_limits",
-           "swof_sync")
+           "swof_sync", "swof_set_halo_push", "swof_ipc_handle", "swof_ipc_open", "swof_ipc_close",
+           "swof_copy")
 SIDE_S, SIDE_N = 2, 3
 
 
@@ -101,6 +102,11 @@ def lib():
         L.swof_refresh_cfl.argtypes = [vp]
         L.swof_set_limits.argtypes = [vp, C.c_double, C.c_int64]
         L.swof_sync.argtypes = [vp]
+        L.swof_set_halo_push.argtypes = [vp, C.c_int32, PD, PD]
+        L.swof_ipc_handle.argtypes = [vp, vp, C.POINTER(C.c_uint64)]
+        L.swof_ipc_open.argtypes = [vp, PD]
+        L.swof_ipc_close.argtypes = [vp]
+        L.swof_copy.argtypes = [vp, vp, C.c_size_t, vp]
         L.swof_destroy.argtypes = [vp]
         L.swof_destroy.restype = None
         L.swof_last_error.argtypes = [vp]
@@ -111,7 +117,8 @@ def lib():
                      "swof_get_state", "swof_get_dt_history", "swof_get_diag", "swof_predictor",
                      "swof_step_profiled", "swof_launches_per_step", "swof_ctx_launches_per_step",
                      "swof_selftest_math", "swof_flow_direction", "swof_flow_direction_f32", "swof_halo_rows",
-                     "swof_enqueue_phase", "swof_cfl_maxima", "swof_refresh_cfl", "swof_set_limits", "swof_sync"):
+                     "swof_enqueue_phase", "swof_cfl_maxima", "swof_refresh_cfl", "swof_set_limits", "swof_sync",
+                     "swof_set_halo_push", "swof_ipc_handle", "swof_ipc_open", "swof_ipc_close", "swof_copy"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -281,6 +288,26 @@ class Solver:
         rv = [self._view(recv[k], nb.value, torch.float64) for k in range(3) if recv[k]]
         return sv, rv
 
+    def set_halo_push(self, side: int, set0_ptrs, set1_ptrs):
+        """Fused exchange: device addresses (ints) of the neighbour's 3 receive blocks per field set."""
+        a = (C.c_void_p * 3)(*set0_ptrs) if set0_ptrs is not None else None
+        b = (C.c_void_p * 3)(*set1_ptrs) if set1_ptrs is not None else None
+        self._check(self._L.swof_set_halo_push(self._ctx, side, a, b))
+
+    def ipc_handle(self):
+        """(64-byte IPC handle of the library-allocated workspace, its base address here)."""
+        h = (C.c_ubyte * 64)()
+        base = C.c_uint64()
+        self._check(self._L.swof_ipc_handle(self._ctx, h, C.byref(base)))
+        return bytes(h), base.value
+
+    def halo_block_addrs(self, field_set: int, side: int):
+        """Device addresses ([send x3], [recv x3]) of the 2-row blocks (see halo_rows)."""
+        send, recv = (C.c_void_p * 3)(), (C.c_void_p * 3)()
+        nb = C.c_size_t()
+        self._check(self._L.swof_halo_rows(self._ctx, field_set, side, send, recv, C.byref(nb)))
+        return [send[k] for k in range(3)], [recv[k] for k in range(3)], nb.value
+
     def enqueue_phase(self, phase: int):
         self._check(self._L.swof_enqueue_phase(self._ctx, phase))
 
@@ -290,6 +317,11 @@ class Solver:
         ptr = C.c_void_p()
         self._check(self._L.swof_cfl_maxima(self._ctx, C.byref(ptr)))
         return self._view(ptr.value, 16, torch.int64)
+
+    def cfl_maxima_addr(self) -> int:
+        ptr = C.c_void_p()
+        self._check(self._L.swof_cfl_maxima(self._ctx, C.byref(ptr)))
+        return ptr.value
 
     def refresh_cfl(self):
         self._check(self._L.swof_refresh_cfl(self._ctx))
@@ -344,3 +376,25 @@ def flow_direction(z, out=None, stream=None):
     if rc != SWOF_OK:
         raise SwofError(rc, L.swof_strerror(rc).decode())
     return out
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a neighbour's workspace (swof_ipc_open); returns its base address in this process."""
+    L = lib()
+    p = C.c_void_p()
+    buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+    rc = L.swof_ipc_open(buf, C.byref(p))
+    if rc != SWOF_OK:
+        raise SwofError(rc, "swof_ipc_open failed")
+    return p.value
+
+
+def ipc_close(base: int):
+    lib().swof_ipc_close(C.c_void_p(base))
+
+
+def copy(dst: int, src: int, nbytes: int, stream=None):
+    """swof_copy: enqueue a copy between device addresses (ints) on `stream` (a torch.cuda.Stream)."""
+    rc = lib().swof_copy(C.c_void_p(dst), C.c_void_p(src), nbytes, C.c_void_p(stream.cuda_stream) if stream else None)
+    if rc != SWOF_OK:
+        raise SwofError(rc, "swof_copy failed")
