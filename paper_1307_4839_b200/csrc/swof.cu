@@ -295,6 +295,7 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     b.fric = has_ff ? (double*)(base + L.off_fric + g) : nullptr;
     b.st = (DevState*)(base + L.off_st);
     std::memset(b.push, 0, sizeof(b.push));
+    b.push_any = 0;
     b.dt_hist = (double*)(base + L.off_hist);
     b.dt_cap = p->dt_hist_cap > 0 ? p->dt_hist_cap : (int64_t)1 << 20;
     c->d_part = (double*)(base + L.off_part);
@@ -579,7 +580,16 @@ int swof_set_halo_push(swof_ctx* c, int32_t side, double* const* set0, double* c
         c->kb.push[s][0][k] = set0 ? set0[k] : nullptr;
         c->kb.push[s][1][k] = set1 ? set1[k] : nullptr;
     }
-    if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }   // kernel params changed
+    c->kb.push_any = 0;
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) c->kb.push_any |= c->kb.push[a][b][0] != nullptr;
+    // the pushing kernels are the generic instance compiled with the fused exchange
+    const bool generic = c->kp.flux != SWOF_FLUX_HLL || c->kp.order == 1 || c->kp.ga_form != SWOF_GA_PRINTED;
+    c->kpred = select_stage<false>(c->kp.fk, c->kp.ga != 0, c->kb.fric != nullptr, generic, c->kb.push_any != 0);
+    c->kcorr = select_stage<true>(c->kp.fk, c->kp.ga != 0, c->kb.fric != nullptr, generic, c->kb.push_any != 0);
+    CK(cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    CK(cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }   // kernels changed
     return SWOF_OK;
 }
 

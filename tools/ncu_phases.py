@@ -83,12 +83,20 @@ for r in csv.reader(io.StringIO(sass)):
         c["inst"] += int(r[h.index("Instructions Executed")] or 0)
         for s in REASONS:
             c[s] += int(r[h.index(s)] or 0)
+        for col, key in (("L1 Wavefronts Shared", "shwf"), ("L1 Wavefronts Shared Excessive", "shex")):
+            try:
+                c[key] += float(r[h.index(col)] or 0)
+            except (ValueError, IndexError):
+                pass
 for k, phs in res.items():
     ts = sum(c["samples"] for c in phs.values())
     ti = sum(c["inst"] for c in phs.values())
     print("==", k[:70])
-    print(f"  {'phase':18s} {'inst%':>6s} {'smpl%':>6s} " + " ".join(f"{s[6:12]:>6s}" for s in REASONS))
+    tw = sum(c["shwf"] for c in phs.values()) or 1.0
+    print(f"  {'phase':18s} {'inst%':>6s} {'smpl%':>6s} " + " ".join(f"{s[6:12]:>6s}" for s in REASONS) +
+          "  shared-wavefronts% (excess%)")
     for ph in [b[0] for b in bounds] + ["helpers (inlined)"]:
         c = phs[ph]
         print(f"  {ph:18s} {100 * c['inst'] / ti:6.1f} {100 * c['samples'] / ts:6.1f} " +
-              " ".join(f"{100 * c[s] / ts:6.1f}" for s in REASONS))
+              " ".join(f"{100 * c[s] / ts:6.1f}" for s in REASONS) +
+              f"  {100 * c['shwf'] / tw:5.1f} ({100 * c['shex'] / tw:4.1f})")
