@@ -264,8 +264,36 @@ def make_cfg4(nx: int = 8192, ny: int = 8192, steps: int = 1000) -> SwofConfig:
 _MAKERS = {"cfg0": make_cfg0, "cfg1": make_cfg1, "cfg2": make_cfg2, "cfg3": make_cfg3, "cfg4": make_cfg4}
 
 
+def _cached(name, nx, ny, kw):
+    """Optional on-disk cache of generated inputs (env SWOF_WORKLOAD_CACHE=dir; used by tools/ab.sh so that
+    repeated bench runs in one GPU session do not regenerate 8192^2 rasters)."""
+    import os
+    import pickle
+    d = os.environ.get("SWOF_WORKLOAD_CACHE")
+    if not d:
+        return None, None
+    os.makedirs(d, exist_ok=True)
+    path = os.path.join(d, f"{name}_{nx}_{ny}_{sorted(kw.items())}.pkl".replace(" ", ""))
+    if os.path.exists(path):
+        with open(path, "rb") as f:
+            return pickle.load(f), path
+    return None, path
+
+
 def make(name: str, nx: Optional[int] = None, ny: Optional[int] = None, **kw) -> SwofConfig:
     """Build workload `name` at full size, or the same recipe at (nx, ny)."""
+    cfg, path = _cached(name, nx, ny, kw)
+    if cfg is not None:
+        return cfg
+    cfg = _make(name, nx, ny, **kw)
+    if path is not None:
+        import pickle
+        with open(path, "wb") as f:
+            pickle.dump(cfg, f, protocol=4)
+    return cfg
+
+
+def _make(name: str, nx: Optional[int] = None, ny: Optional[int] = None, **kw) -> SwofConfig:
     fn = _MAKERS[name]
     if nx is not None:
         kw["nx"] = nx
