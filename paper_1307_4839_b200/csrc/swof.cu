@@ -332,6 +332,13 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     c->kcorr = select_stage<true>(k.fk, k.ga != 0, has_ff, generic);
     cudaError_t e = cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    {   // resident CTAs of the stage kernel: the distance of the next-tile L2 prefetch
+        int per_sm = 0, dev = 0, sms = 0;
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kpred, NT, SMEM_BYTES);
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        k.pf_stride = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 1);
+    }
     if (e == cudaSuccess) e = cudaMemsetAsync(c->ws, 0, L.total, c->stream);
     if (e != cudaSuccess) { int rc = cuda_fail(c, e, "swof_create"); fprintf(stderr, "swof: %s\n", c->err.c_str()); swof_destroy(c); return rc; }
     int rc = copy_field_in(c, b.z, z);

@@ -75,8 +75,12 @@ for r in csv.reader(io.StringIO(sass)):
         base = a if base is None else base
         # the instance's mangled name from the template arguments in the demangled kernel name
         args = [int(x) for x in re.findall(r"\((?:bool|int)\)(\d+)", kern)]
-        fn = ("_ZN4swof12stage_kernelILb%dENS_4PhysILi%dELb%dELb%dEEEEEvNS_7KParamsENS_5KBufsEi" % tuple(args)
-              if len(args) == 4 else "_ZN4swof12stage_kernelILb%dEEEvNS_7KParamsENS_5KBufsEi" % args[0])
+        if len(args) == 5:
+            fn = "_ZN4swof12stage_kernelILb%dENS_4PhysILi%dELb%dELb%dEEELb%dEEEvNS_7KParamsENS_5KBufsEi" % tuple(args)
+        elif len(args) == 4:
+            fn = "_ZN4swof12stage_kernelILb%dENS_4PhysILi%dELb%dELb%dEEEEEvNS_7KParamsENS_5KBufsEi" % tuple(args)
+        else:
+            fn = "_ZN4swof12stage_kernelILb%dEEEvNS_7KParamsENS_5KBufsEi" % args[0]
         ph = phase_of(lines.get((fn, a - base)))
         c = res[kern][ph]
         c["samples"] += int(r[h.index("# Samples")] or 0)
