@@ -16,6 +16,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import subprocess
 import sys
 import threading
@@ -310,7 +311,7 @@ def main():
             with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
                 prof = json.load(f)
             for kname, k in prof["kernels"].items():
-                is_corr = "stage_kernel<(bool)1" in kname or "stage_kernel<1>" in kname or "<true" in kname
+                is_corr = re.search(r"stage_kernel<(\(bool\))?(1|true)\b", kname) is not None
                 if is_corr == (dom == "corrector"):
                     traffic = k["dram_bytes_per_cell"] * cells
                     tsrc = f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"
