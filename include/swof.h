@@ -179,6 +179,10 @@ int swof_get_diag(swof_ctx* c, swof_diag* d);
 int swof_predictor(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf);
 int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms);
 
+/* Bounds-checked builds (-DSWOF_CHECK=1): the source line of the first failed index check in
+ * csrc/swof_kernels.cuh since the library was loaded, 0 if none (always 0 in normal builds), -1 on error. */
+int swof_check_line(void);
+
 /* Number of kernel launches one time step issues with the default scheme (2: predictor and
  * corrector).  swof_ctx_launches_per_step: the same for a context's scheme (2, or 3 with SWOF_CFL_FACE:
  * the reconstructed-value CFL maxima are a separate stencil pass). */

@@ -35,10 +35,12 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, defines=()) -> Path:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path = LIB) -> Path:
+    """Compile the library (out: another file for a diagnostic build, e.g. -DSWOF_CHECK=1)."""
+    out = Path(out)
+    if out == LIB and not force and not stale():
         return LIB
-    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+    tmp = out.with_suffix(f".so.tmp{os.getpid()}")
     cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", str(tmp), *map(str, SOURCES), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -46,9 +48,10 @@ def build(force: bool = False, verbose: bool = False, defines=()) -> Path:
         raise RuntimeError(f"nvcc failed ({r.returncode}): {' '.join(cmd)}")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    (PKG / "libswof.ptxas.txt").write_text(r.stderr)
-    return LIB
+    os.replace(tmp, out)
+    if out == LIB:
+        (PKG / "libswof.ptxas.txt").write_text(r.stderr)
+    return out
 
 
 if __name__ == "__main__":

@@ -223,6 +223,12 @@ __global__ void fill_kernel(double* a, int nx, int ny, int pitch, double v) {
 extern "C" {
 
 int swof_launches_per_step(void) { return 2; }
+
+int swof_check_line(void) {
+    int line = 0;
+    if (cudaMemcpyFromSymbol(&line, g_swof_assert_line, sizeof(int)) != cudaSuccess) return -1;
+    return line;
+}
 int swof_ctx_launches_per_step(const swof_ctx* c) { return c ? 2 + (c->kp.cfl_mode == SWOF_CFL_FACE ? 1 : 0) : -1; }
 
 int swof_selftest_math(int64_t n, uint64_t seed, int64_t* mismatches) {

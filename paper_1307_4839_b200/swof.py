@@ -11,7 +11,10 @@ from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "libswof.so"
+import os
+
+# SWOF_LIB: an alternative build of the same library (tests: the bounds-checked -DSWOF_CHECK=1 build)
+_LIB_PATH = Path(os.environ.get("SWOF_LIB", Path(__file__).resolve().parent / "libswof.so"))
 
 SWOF_OK, SWOF_EINVAL, SWOF_ENUMERIC, SWOF_ECUDA, SWOF_ENOMEM, SWOF_ESTATE = range(6)
 FRIC = {"none": 0, "manning": 1, "strickler": 2, "darcy_weisbach": 3, "chezy": 4}
@@ -28,7 +31,7 @@ EXPORTS = ("swof_workspace_size", "swof_create", "swof_set_state", "swof_step", 
            "swof_last_error", "swof_strerror", "swof_flow_direction", "swof_flow_direction_f32",
            "swof_halo_rows", "swof_enqueue_phase", "swof_cfl_maxima", "swof_refresh_cfl", "swof_set_limits",
            "swof_sync", "swof_set_halo_push", "swof_ipc_handle", "swof_ipc_open", "swof_ipc_close",
-           "swof_copy")
+           "swof_copy", "swof_check_line")
 SIDE_S, SIDE_N = 2, 3
 
 
@@ -107,6 +110,7 @@ def lib():
         L.swof_ipc_open.argtypes = [vp, PD]
         L.swof_ipc_close.argtypes = [vp]
         L.swof_copy.argtypes = [vp, vp, C.c_size_t, vp]
+        L.swof_check_line.argtypes = []
         L.swof_destroy.argtypes = [vp]
         L.swof_destroy.restype = None
         L.swof_last_error.argtypes = [vp]
@@ -118,7 +122,8 @@ def lib():
                      "swof_step_profiled", "swof_launches_per_step", "swof_ctx_launches_per_step",
                      "swof_selftest_math", "swof_flow_direction", "swof_flow_direction_f32", "swof_halo_rows",
                      "swof_enqueue_phase", "swof_cfl_maxima", "swof_refresh_cfl", "swof_set_limits", "swof_sync",
-                     "swof_set_halo_push", "swof_ipc_handle", "swof_ipc_open", "swof_ipc_close", "swof_copy"):
+                     "swof_set_halo_push", "swof_ipc_handle", "swof_ipc_open", "swof_ipc_close", "swof_copy",
+                     "swof_check_line"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
