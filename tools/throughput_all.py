@@ -1,0 +1,45 @@
+"""CUDA-event throughput of the time step on every BASELINE.json configuration at full size (SURVEY.md §4
+T6), plus the scheme variants on cfg4: one JSON line per case (cell-updates/s, ms per step, kernel split)."""
+import json
+import sys
+import time
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+
+from paper_1307_4839_b200 import Solver, params_from_config  # noqa: E402
+from workloads import make  # noqa: E402
+
+torch.cuda.set_device(0)
+CASES = [("cfg4", {"flux": "rusanov", "cfl": 0.25}, 50), ("cfg4", {"order": 1, "cfl": 1.0}, 50),
+         ("cfg4", {"cfl_mode": "face"}, 50), ("cfg4", {"ga_form": "darcy"}, 50)] if "--variants" in sys.argv else [
+         ("cfg0", {}, 200), ("cfg1", {}, 200), ("cfg2", {}, 100), ("cfg3", {}, 100), ("cfg4", {}, 50),
+         ("cfg4", {"flux": "rusanov", "cfl": 0.25}, 50), ("cfg4", {"order": 1, "cfl": 1.0}, 50),
+         ("cfg4", {"cfl_mode": "face"}, 50), ("cfg4", {"ga_form": "darcy"}, 50)]
+for name, kw, steps in CASES:
+    t0 = time.time()
+    cfg = make(name)
+    for k, v in kw.items():
+        setattr(cfg, k, v)
+    cfg.clamp_fail = 1.0 if kw else 0.0   # variants: report throughput even where the variant clamps (DESIGN Q23)
+    stream = torch.cuda.Stream()
+    s = Solver(params_from_config(cfg), cfg.z, cfg.fric_field, stream=stream)
+    s.set_state(cfg.h, cfg.hu, cfg.hv, cfg.vinf if cfg.ga is not None else None, 0.0)
+    s.step(5)
+    if name in ("cfg2", "cfg3"):
+        s.step(50)                      # let water enter the initially dry domains
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    s.step(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    kp = s.step_profiled(min(steps, 10))
+    d = s.diag()
+    print(json.dumps({"case": name, "variant": kw, "nx": cfg.nx, "ny": cfg.ny, "steps": steps,
+                      "cell_updates_per_s": cfg.nx * cfg.ny * steps / (ms / 1e3), "ms_per_step": ms / steps,
+                      "kernel_ms_per_step": [x / min(steps, 10) for x in kp], "wet_cells": d["wet_cells"],
+                      "launches_per_step": s.launches_per_step(), "setup_s": round(time.time() - t0, 1)}),
+          flush=True)
+    s.close()
