@@ -36,6 +36,7 @@ struct swof_ctx {
     int diag_blocks = 0;
     dim3 grid;
     StageFn kpred = nullptr, kcorr = nullptr;   // stage kernel instances for this context's physics
+    dim3 cf_grid;                               // face-CFL pass tiles
     std::string err;
 };
 
@@ -140,7 +141,7 @@ constexpr int PW_BLOCKS = 1184;        // point-wise / face-CFL passes: 8 CTAs x
 void launch_second(swof_ctx* c, int par, cudaStream_t s) {
     if (c->kp.order == 1) euler_commit_kernel<<<PW_BLOCKS, PW_NT, 0, s>>>(c->kp, c->kb, par);
     else c->kcorr<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
-    if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<PW_BLOCKS, PW_NT, 0, s>>>(c->kp, c->kb, par, 0);
+    if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<c->cf_grid, dim3(CF_TX, CF_NTY), 0, s>>>(c->kp, c->kb, par, 0);
 }
 void launch_step(swof_ctx* c, int par, cudaStream_t s) {
     c->kpred<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
@@ -332,6 +333,7 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     }
     c->grid = dim3((unsigned)((p->nx + TX - 1) / TX), (unsigned)((p->ny + TY - 1) / TY));
     c->diag_blocks = DIAG_BLOCKS;
+    c->cf_grid = dim3((unsigned)((p->nx + CF_TX - 1) / CF_TX), (unsigned)((p->ny + CF_TY - 1) / CF_TY));
 
     const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
     c->kpred = select_stage<false>(k.fk, k.ga != 0, has_ff, generic);
@@ -385,7 +387,7 @@ int swof_set_state(swof_ctx* c, const double* h, const double* hu, const double*
     init_cfl_kernel<<<1184, 256, 0, c->stream>>>(c->kp, c->kb);
     if (c->kp.cfl_mode == SWOF_CFL_FACE) {               // replace the cell maxima by the face ones
         CK(cudaMemsetAsync(&c->kb.st->amax[0][0], 0, 2 * sizeof(unsigned long long), c->stream));
-        cfl_face_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, 0, 1);
+        cfl_face_kernel<<<c->cf_grid, dim3(CF_TX, CF_NTY), 0, c->stream>>>(c->kp, c->kb, 0, 1);
     }
     CK(cudaGetLastError());
     c->par = 0;
@@ -645,7 +647,7 @@ int swof_enqueue_phase(swof_ctx* c, int32_t phase) {
         if (c->kp.order == 1) euler_commit_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, c->par);
         else c->kcorr<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
     } else if (phase == 2) {
-        if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, c->par, 0);
+        if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<c->cf_grid, dim3(CF_TX, CF_NTY), 0, c->stream>>>(c->kp, c->kb, c->par, 0);
         c->par ^= 1;                          // the step is complete
     } else {
         return fail(c, SWOF_EINVAL, "phase must be 0, 1 or 2");
@@ -665,7 +667,7 @@ int swof_refresh_cfl(swof_ctx* c) {
     if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_refresh_cfl before swof_set_state");
     if (c->par != 0) return fail(c, SWOF_ESTATE, "swof_refresh_cfl only right after swof_set_state");
     CK(cudaMemsetAsync(&c->kb.st->amax[0][0], 0, 2 * sizeof(unsigned long long), c->stream));
-    if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, 0, 1);
+    if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<c->cf_grid, dim3(CF_TX, CF_NTY), 0, c->stream>>>(c->kp, c->kb, 0, 1);
     else init_cfl_kernel<<<1184, 256, 0, c->stream>>>(c->kp, c->kb);
     CK(cudaGetLastError());
     return SWOF_OK;
