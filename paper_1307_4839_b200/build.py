@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: Path = LI
     if out == LIB and not force and not stale():
         return LIB
     tmp = out.with_suffix(f".so.tmp{os.getpid()}")
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", str(tmp), *map(str, SOURCES), "-lcudart"]
+    extra = os.environ.get("SWOF_NVCC_EXTRA", "").split()        # A/B experiments (tools/ab.sh) only
+    cmd = [NVCC, *NVCC_FLAGS, *extra, *[f"-D{d}" for d in defines], "-o", str(tmp), *map(str, SOURCES), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

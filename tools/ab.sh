@@ -9,7 +9,9 @@ mkdir -p gpurun_out
 export SWOF_WORKLOAD_CACHE=/tmp/swof_wl_cache
 i=0
 for v in "$@"; do
-  python -m paper_1307_4839_b200.build --force $v > gpurun_out/ab_build_$i.log 2>&1 || echo "variant $i build failed" >> gpurun_out/ab.log
+  # a variant is "-DNAME=V ..." defines, optionally with nvcc flags after "::" ("-DX=1 :: -Xptxas -dlcm=cg")
+  defs="${v%%::*}"; extra=""; [[ "$v" == *::* ]] && extra="${v#*::}"
+  SWOF_NVCC_EXTRA="$extra" python -m paper_1307_4839_b200.build --force $defs > gpurun_out/ab_build_$i.log 2>&1 || echo "variant $i build failed" >> gpurun_out/ab.log
   cp paper_1307_4839_b200/libswof.so gpurun_out/ab_$i.so
   i=$((i+1))
 done
