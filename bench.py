@@ -315,6 +315,10 @@ def main():
                 if is_corr == (dom == "corrector"):
                     traffic = k["dram_bytes_per_cell"] * cells
                     tsrc = f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"
+                    out["ncu_dominant_kernel"] = {  # context from the same capture: what bounds the kernel
+                        "fp64_pipe_pct": k.get("fp64_pipe_pct"), "issue_active_pct": k.get("issue_active_pct"),
+                        "dram_throughput_pct": k.get("dram_throughput_pct"), "registers": k.get("registers"),
+                        "warps_active_pct": k.get("warps_active_pct")}
         except Exception:
             pass
         out["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak_gops, "unit": "Gop/s (fp64)",
