@@ -1,6 +1,6 @@
 #!/bin/bash
 # build + time kernel variants on the GPU box:
-#   bash tools/variants.sh "-DSWOF_MIN_BLOCKS=2" "ALT:v4" ...
+#   bash tools/variants.sh "-DSWOF_MIN_BLOCKS=2" ...  (tools/ab.sh interleaves rounds: prefer it)
 # "ALT:<name>" builds tools/alt/<name>/swof.cu (a frozen earlier kernel) instead of the tree's sources.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
