@@ -5,6 +5,7 @@ import sys
 import time
 
 sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
 import torch  # noqa: E402
 
 from paper_1307_4839_b200 import Solver, params_from_config  # noqa: E402
@@ -37,7 +38,21 @@ for name, kw, steps in CASES:
     ms = e0.elapsed_time(e1)
     kp = s.step_profiled(min(steps, 10))
     d = s.diag()
-    print(json.dumps({"case": name, "variant": kw, "nx": cfg.nx, "ny": cfg.ny, "steps": steps,
+    rate = cfg.nx * cfg.ny * steps / (ms / 1e3)
+    roof = {}
+    if not kw:
+        # rooflines as bench.py computes them for cfg4: HBM (algorithmic bytes of the per-stage design) and
+        # fp64 lanes (algorithmic ops per cell-update from the oracle's branch counters on a centre crop)
+        import bench
+        peaks, src = bench.load_peaks()
+        bp, bc = bench.bytes_per_cell_update(cfg.ga is not None, cfg.fric_field is not None)
+        crop = min(256, cfg.nx, cfg.ny)
+        _, cnt, _, nst = bench.cpu_sample(cfg, crop, 4)
+        f_alg = bench.f_alg_from_counters(cnt, cfg, nst, crop * crop)
+        peak_gops = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+        roof = {"bytes_per_cell_update": bp + bc, "hbm_frac": (bp + bc) * rate / 1e9 / peaks["hbm_gbs"],
+                "f_alg_per_cell_update": f_alg, "alu_frac": f_alg * rate / 1e9 / peak_gops, "peak_source": src}
+    print(json.dumps({"case": name, "variant": kw, "nx": cfg.nx, "ny": cfg.ny, "steps": steps, "roofline": roof,
                       "cell_updates_per_s": cfg.nx * cfg.ny * steps / (ms / 1e3), "ms_per_step": ms / steps,
                       "kernel_ms_per_step": [x / min(steps, 10) for x in kp], "wet_cells": d["wet_cells"],
                       "launches_per_step": s.launches_per_step(), "setup_s": round(time.time() - t0, 1)}),

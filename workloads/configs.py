@@ -69,6 +69,7 @@ class SwofConfig:
     order: int = 2                                 # 2: MUSCL + Heun | 1: first order, explicit Euler
     cfl_mode: str = "cell"                         # "cell" (Q10) | "face": reconstructed values
     ga_form: str = "printed"                       # "printed" | "darcy": h_f + h_over (Q15)
+    clamp_fail: float = 0.0                        # largest tolerated single clamp [m] (0: library default)
     steps: Optional[int] = None                    # fixed step count (swof_step), or
     t_end: Optional[float] = None                  # run to t_end (swof_run)
     # inputs
