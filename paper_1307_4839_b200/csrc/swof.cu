@@ -336,8 +336,8 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     c->cf_grid = dim3((unsigned)((p->nx + CF_TX - 1) / CF_TX), (unsigned)((p->ny + CF_TY - 1) / CF_TY));
 
     const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
-    c->kpred = select_stage<false>(k.fk, k.ga != 0, has_ff, generic);
-    c->kcorr = select_stage<true>(k.fk, k.ga != 0, has_ff, generic);
+    c->kpred = select_stage<false>(k.fk, k.ga != 0, has_ff, generic, false, p->dry_skip != 0);
+    c->kcorr = select_stage<true>(k.fk, k.ga != 0, has_ff, generic, false, p->dry_skip != 0);
     cudaError_t e = cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     {   // resident CTAs of the stage kernel: the distance of the next-tile L2 prefetch
@@ -600,8 +600,10 @@ int swof_set_halo_push(swof_ctx* c, int32_t side, double* const* set0, double* c
         for (int b = 0; b < 2; ++b) c->kb.push_any |= c->kb.push[a][b][0] != nullptr;
     // the pushing kernels are the generic instance compiled with the fused exchange
     const bool generic = c->kp.flux != SWOF_FLUX_HLL || c->kp.order == 1 || c->kp.ga_form != SWOF_GA_PRINTED;
-    c->kpred = select_stage<false>(c->kp.fk, c->kp.ga != 0, c->kb.fric != nullptr, generic, c->kb.push_any != 0);
-    c->kcorr = select_stage<true>(c->kp.fk, c->kp.ga != 0, c->kb.fric != nullptr, generic, c->kb.push_any != 0);
+    c->kpred = select_stage<false>(c->kp.fk, c->kp.ga != 0, c->kb.fric != nullptr, generic, c->kb.push_any != 0,
+                                   c->p.dry_skip != 0);
+    c->kcorr = select_stage<true>(c->kp.fk, c->kp.ga != 0, c->kb.fric != nullptr, generic, c->kb.push_any != 0,
+                                  c->p.dry_skip != 0);
     CK(cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
     CK(cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
     if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }   // kernels changed

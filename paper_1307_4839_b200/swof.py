@@ -48,7 +48,7 @@ class SwofParams(C.Structure):
         ("n_hydro", C.c_int32 * 4), ("hydro_t", (C.c_double * MAXT) * 4), ("hydro_q", (C.c_double * MAXT) * 4),
         ("dt_hist_cap", C.c_int64), ("graph_steps", C.c_int32), ("clamp_fail", C.c_double),
         ("flux", C.c_int32), ("order", C.c_int32), ("cfl_mode", C.c_int32), ("ga_form", C.c_int32),
-        ("inflow_width", C.c_double * 4),
+        ("inflow_width", C.c_double * 4), ("dry_skip", C.c_int32),
     ]
 
 
@@ -157,6 +157,7 @@ def params_from_config(cfg, graph_steps: int = 0, dt_hist_cap: int = 0) -> SwofP
     p.cfl_mode = CFL_MODE[getattr(cfg, "cfl_mode", "cell")]
     p.ga_form = GA_FORM[getattr(cfg, "ga_form", "printed")]
     p.clamp_fail = float(getattr(cfg, "clamp_fail", 0.0))
+    p.dry_skip = int(bool(getattr(cfg, "dry_skip", False)))
     return p
 
 

@@ -19,6 +19,7 @@ VARIANTS = {
     "cflface": dict(cfl_mode="face"),
     "darcyga": dict(ga_form="darcy"),
     "all": dict(flux="rusanov", order=1, cfl=1.0, cfl_mode="face", ga_form="darcy"),
+    "dryskip": dict(dry_skip=True),          # GPU-only optimisation: results must not change
 }
 CASES = [("cfg0", 64, 64), ("cfg1", 100, 70), ("cfg3", 130, 90), ("cfg4", 75, 41)]
 
@@ -100,3 +101,18 @@ def test_variant_launch_counts(gpu):
         s = gpu_solver(variant_cfg("cfg0", 64, 64, VARIANTS[vname], 1))
         assert s.launches_per_step() == n, vname
         s.close()
+
+
+@pytest.mark.parametrize("name,nx,ny", [("cfg2", 97, 53), ("cfg3", 130, 90)])
+def test_dry_skip_on_drying_domains(gpu, name, nx, ny):
+    """Mostly dry domains (rain infiltrating, an inflow front): the all-dry tiles take the skip path."""
+    cfg = make(name, nx=nx, ny=ny)
+    cfg.steps, cfg.t_end = 200, None
+    base = gpu_run(cfg, nsteps=200)
+    cfg.dry_skip = True
+    fast = gpu_run(cfg, nsteps=200)
+    for k in ("h", "hu", "hv", "v"):
+        assert np.array_equal(fast[k], base[k]), k
+    assert np.array_equal(fast["dt"], base["dt"])
+    r = oracle.run(cfg)
+    compare(fast, r, TOL_FULL)

@@ -70,6 +70,7 @@ class SwofConfig:
     cfl_mode: str = "cell"                         # "cell" (Q10) | "face": reconstructed values
     ga_form: str = "printed"                       # "printed" | "darcy": h_f + h_over (Q15)
     clamp_fail: float = 0.0                        # largest tolerated single clamp [m] (0: library default)
+    dry_skip: bool = False                         # GPU: skip the stencil work of all-dry tiles (results unchanged)
     steps: Optional[int] = None                    # fixed step count (swof_step), or
     t_end: Optional[float] = None                  # run to t_end (swof_run)
     # inputs
