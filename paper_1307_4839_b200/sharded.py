@@ -133,12 +133,16 @@ class IpcExchanger:
     """One strip per process, the neighbours' workspaces mapped with CUDA IPC (NVLink peer memory across
     GPUs; also valid between processes sharing one GPU).  Fused mode only: the kernels push boundary rows
     into the mapped neighbours; the state loaded by set_state is pulled once by copies.  Ordering between
-    strips is a host barrier after each phase (torch.distributed, any backend) and the CFL all-reduce is
-    host-staged -- correct by construction; an in-stream NCCL barrier is the faster production variant."""
+    strips after each phase is either a host barrier (any backend: stream synchronise + dist.barrier; the
+    mode the tests run, 2-3 processes sharing one GPU over gloo) or, with in_stream=True on an NCCL group,
+    a one-word all-reduce enqueued on the strip's stream (no host round trip: the neighbours' producing
+    kernels precede their all-reduce in stream order, so its completion orders their peer stores before
+    this strip's next phase); the CFL all-reduce follows the same choice."""
 
-    def __init__(self, rank: int, nranks: int, group=None):
-        self.rank, self.nranks, self.group = rank, nranks, group
+    def __init__(self, rank: int, nranks: int, group=None, in_stream: bool = False):
+        self.rank, self.nranks, self.group, self.in_stream = rank, nranks, group, in_stream
         self.peers = {}                       # side -> (mapped base, info dict of the neighbour)
+        self._word = None                     # device scratch of the in-stream barrier / CFL all-reduce
 
     def _neighbours(self):
         out = {}
@@ -181,8 +185,21 @@ class IpcExchanger:
                     dev_copy(dst, mbase + off, nb, sv.stream)
         self.barrier(strips)
 
+    def _scratch(self, sv):
+        import torch
+        if self._word is None:
+            self._word = torch.zeros(3, dtype=torch.int64, device=torch.cuda.current_device())
+        return self._word
+
     def barrier(self, strips):
+        import torch
         import torch.distributed as dist
+        if self.in_stream and self.nranks > 1:
+            (sv,) = strips
+            w = self._scratch(sv)
+            with torch.cuda.stream(sv.stream):
+                dist.all_reduce(w[2:3], op=dist.ReduceOp.MAX, group=self.group)
+            return
         for sv in strips:
             sv.stream.synchronize()
         dist.barrier(group=self.group)
@@ -194,6 +211,13 @@ class IpcExchanger:
         if self.nranks == 1:
             return
         addr = sv.cfl_maxima_addr()
+        if self.in_stream:
+            w = self._scratch(sv)
+            with torch.cuda.stream(sv.stream):
+                dev_copy(w.data_ptr(), addr, 16, sv.stream)
+                dist.all_reduce(w[0:2], op=dist.ReduceOp.MAX, group=self.group)
+                dev_copy(addr, w.data_ptr(), 16, sv.stream)
+            return
         host = torch.zeros(2, dtype=torch.int64)
         dev_copy(host.data_ptr(), addr, 16, sv.stream)
         sv.stream.synchronize()
