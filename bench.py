@@ -179,6 +179,9 @@ def main():
     ap.add_argument("--cpu-crop", type=int, default=1024)
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--workload", default="swof", choices=("swof", "d8"))
+    ap.add_argument("--shard-fused", action="store_true",
+                    help="with --shard: fused exchange (kernels push boundary rows into the neighbours' "
+                         "CUDA-IPC-mapped ghost rows) and in-stream NCCL barriers")
     ap.add_argument("--shard", action="store_true",
                     help="N > 1: split the one grid into row strips over the ranks (strong scaling, NCCL halo "
                          "exchange + CFL all-reduce per step) instead of N independent replicas")
@@ -339,7 +342,7 @@ def bench_shard(args, rank, world, local):
     slowest rank's time."""
     import torch
     import torch.distributed as dist
-    from paper_1307_4839_b200.sharded import DistExchanger, ShardedSolver
+    from paper_1307_4839_b200.sharded import DistExchanger, IpcExchanger, ShardedSolver
     from workloads import make
     if world > 1:
         torch.cuda.set_device(local)
@@ -349,7 +352,10 @@ def bench_shard(args, rank, world, local):
     cfg = make(args.config, nx=args.nx, ny=args.ny)
     cells = cfg.nx * cfg.ny
     stream = torch.cuda.Stream()
-    s = ShardedSolver(cfg, world, [rank], DistExchanger(rank, world), stream=stream)
+    if args.shard_fused:
+        s = ShardedSolver(cfg, world, [rank], IpcExchanger(rank, world, in_stream=True), stream=stream, fused=True)
+    else:
+        s = ShardedSolver(cfg, world, [rank], DistExchanger(rank, world), stream=stream)
     s.set_state(cfg.h, cfg.hu, cfg.hv, cfg.vinf if cfg.ga is not None else None, 0.0)
     s.step(args.warmup)
     if world > 1:
@@ -372,7 +378,9 @@ def bench_shard(args, rank, world, local):
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded cfg4 recipe, SURVEY.md §8d)",
                "config": {"workload": args.config, "nx": cfg.nx, "ny": cfg.ny, "cells": cells,
-                          "parallelism": f"row strips x{world} (NCCL halo exchange + CFL all-reduce)",
+                          "parallelism": f"row strips x{world} (" + ("fused IPC halo push + NCCL barriers"
+                                                                     if args.shard_fused else
+                                                                     "NCCL halo exchange") + " + CFL all-reduce)",
                           "l2": "inputs larger than L2; no flush"},
                "gpu_launches": args.steps * (2 + (cfg.cfl_mode == "face")), "clocks": clk.summary(),
                "t": st["t"], "step": st["step"]}

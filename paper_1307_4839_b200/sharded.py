@@ -155,6 +155,8 @@ class IpcExchanger:
     def link_push(self, strips):
         import torch.distributed as dist
         (sv,) = strips
+        if self.nranks == 1:
+            return
         handle, base = sv.ipc_handle()
         info = {"handle": handle, "base": base, "blocks": {}}
         for side in (SIDE_S, SIDE_N):
@@ -194,7 +196,9 @@ class IpcExchanger:
     def barrier(self, strips):
         import torch
         import torch.distributed as dist
-        if self.in_stream and self.nranks > 1:
+        if self.nranks == 1:
+            return
+        if self.in_stream:
             (sv,) = strips
             w = self._scratch(sv)
             with torch.cuda.stream(sv.stream):
