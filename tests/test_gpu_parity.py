@@ -112,14 +112,16 @@ def test_stage_3x3_pin_on_gpu(gpu):
     assert abs(g["hu"][1, 0] - ref["hu_west_edge_centre"] / 2) <= 1e-15
 
 
-def test_full_size_sampled(gpu):
-    """cfg4 at its full 8192^2 size in the bench's launch configuration: after 20 steps, one more step
-    checked cell by cell on sampled cells (interior, walls, corners, wet/dry fronts) against the oracle
-    run on the surrounding 13x13 patch with the GPU's dt; the dt itself against the oracle CFL of the
-    whole state."""
-    cfg = make("cfg4")
+@pytest.mark.parametrize("name,pre_steps", [("cfg1", 30), ("cfg2", 60), ("cfg3", 60), ("cfg4", 20)])
+def test_full_size_sampled(gpu, name, pre_steps):
+    """Every BASELINE.json configuration at its full size, in the bench's launch configuration: after
+    `pre_steps` steps, one more step checked cell by cell on sampled cells (corners, edges, the cfg3 inflow
+    segment, random cells, wet/dry fronts) against the oracle run on the surrounding 13x13 patch with the
+    GPU's dt; the dt itself against the oracle CFL of the whole state."""
+    cfg = make(name)
+    cfg.steps, cfg.t_end = None, None
     s = gpu_solver(cfg)
-    s.step(20)
+    s.step(pre_steps)
     st = s.get_state()
     P = oracle.params_from_config(cfg)
     dt_or, _, _ = oracle.cfl_dt(P, st["h"], st["hu"], st["hv"], st["t"])
@@ -128,22 +130,30 @@ def test_full_size_sampled(gpu):
     dt_gpu = s.dt_history()[-1]
     assert abs(dt_gpu / dt_or - 1) <= 1e-13
     rng = np.random.default_rng(1307)
-    n = cfg.nx
-    pts = [(0, 0), (n - 1, n - 1), (0, n - 1), (n - 1, 0), (1, 4000), (4000, 1), (n - 2, 777), (31, 15), (32, 16)]
-    pts += [tuple(x) for x in rng.integers(0, n, size=(40, 2))]
-    front = np.argwhere((st["h"][1:-1, 1:-1] > 1e-12) != (st["h"][1:-1, 2:] > 1e-12))
-    pts += [(int(b) + 1, int(a) + 1) for a, b in front[rng.choice(len(front), 10, replace=False)]]
+    nx, ny = cfg.nx, cfg.ny
+    pts = [(0, 0), (nx - 1, ny - 1), (0, ny - 1), (nx - 1, 0), (1, ny // 2), (nx // 2, 1), (nx - 2, 777 % ny),
+           (31, 15), (32, 16), (nx // 2, ny - 1)]
+    pts += [(int(a), int(b)) for a, b in zip(rng.integers(0, nx, 40), rng.integers(0, ny, 40))]
+    for side, fl in cfg.inflow.items():                 # the inflow segment and its ends
+        if side == "W":
+            pts += [(0, fl.k0), (0, (fl.k0 + fl.k1) // 2), (0, fl.k1 - 1), (1, fl.k0 - 1), (2, fl.k1)]
+    wet = st["h"] > 1e-12
+    front = np.argwhere(wet[1:-1, 1:-1] != wet[1:-1, 2:])
+    if len(front):
+        pts += [(int(b) + 1, int(a) + 1) for a, b in front[rng.choice(len(front), min(10, len(front)), replace=False)]]
     worst = 0.0
     bit = True
     for (i, j) in pts:
         sl, r, valid = oracle_patch_step(cfg, st, st["t"], dt_gpu, i, j)
         for k in ("h", "hu", "hv", "v"):
+            if k == "v" and cfg.ga is None:
+                continue
             d = np.abs(g[k][sl] - r[k])[valid]
             worst = max(worst, float(d.max()))
             bit &= bool(np.all(g[k][sl][valid] == r[k][valid]))
     s.close()
     assert worst <= TOL_STEP, worst
-    print("full-size sampled: worst", worst, "bitwise", bit)
+    print(name, "full-size sampled:", len(pts), "cells, worst", worst, "bitwise", bit)
 
 
 # ---------------------------------------------------------------- edge cases
