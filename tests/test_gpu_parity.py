@@ -264,3 +264,30 @@ def test_mass_conservation_gpu(gpu):
     d = s.diag()
     assert abs(d["volume"] - v0) <= 1e-12 * v0 and d["clamps"] == 0 and d["flags"] == 0
     s.close()
+
+
+def test_full_size_full_count_cfg4_budget(gpu):
+    """cfg4 at 8192^2 over its full 1000 steps (the oracle cannot follow that far cell by cell): the
+    properties that hold at any size -- the 4-term water budget of a walled domain with rain and Green-Ampt
+    (sum(h + V) dx dy grows by the Heun-averaged rain, plus half the clamped mass) to
+    1e-12 relative, h >= 0, no flag raised, and the dt history (finite, positive, <= dt_max)."""
+    cfg = make("cfg4")
+    s = gpu_solver(cfg)
+    d0 = s.diag()
+    w0 = d0["volume"] + d0["vinf_volume"]
+    s.step(cfg.steps)
+    d = s.diag()
+    dts = s.dt_history()
+    s.close()
+    assert d["step"] == cfg.steps and d["flags"] == 0 and d["h_min"] >= 0.0
+    t, rain = 0.0, 0.0
+    R = cfg.rain_rate[0]                                  # constant rain on [0, inf)
+    for dt in dts:
+        rain += dt * (R + R) * 0.5
+        t += dt
+    assert t == d["t"] and len(dts) == cfg.steps and np.all(dts > 0) and np.all(dts <= cfg.dt_max)
+    area = cfg.dx * cfg.dy
+    w1 = d["volume"] + d["vinf_volume"]
+    budget = w0 + rain * cfg.cells * area + 0.5 * d["clamped_mass"] * area
+    assert abs(w1 - budget) <= 1e-12 * w1, (w1, budget)
+    assert d["clamped_mass"] * area <= 1e-12 * w1
