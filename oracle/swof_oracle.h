@@ -12,8 +12,12 @@
  *
  * Citations: "P:n" = line n of /root/reference/PAPER.md (read at development time only).
  * Readings of points the paper leaves open are SURVEY.md §8c Q1..Q21, restated in DESIGN.md §3.
- * Parity-unpinned conventions (pinned only by invariants): transverse HLL (Q2), cell-centred CFL (Q10),
- * Green-Ampt sign/V0 (Q15), inflow ghost (Q18), canonical inverse cube root (Q20).
+ * Pins (tests/): the transverse HLL component (Q2) by the hand-derived face pin with a
+ * transverse velocity (golden face_pins.json), both CFL forms (Q10, Q22) by closed forms (3x3 stage,
+ * face-CFL worked example), Green-Ampt as printed and in the Darcy form (Q15) by SPEC examples and
+ * hand-derived capacities, the inflow ghost's discharge (Q18) by the inflow mass rate, icbrt (Q20) by libm
+ * cbrt to 2 ulp.  Pinned only by invariants ("parity unpinned" otherwise): the critical-depth height h_c
+ * of the inflow ghost (Q18) and the choice V0 = 3 mm (Q15), both problem data rather than arithmetic.
  */
 #ifndef SWOF_ORACLE_H
 #define SWOF_ORACLE_H
