@@ -15,9 +15,9 @@
  * Pins (tests/): the transverse HLL component (Q2) by the hand-derived face pin with a
  * transverse velocity (golden face_pins.json), both CFL forms (Q10, Q22) by closed forms (3x3 stage,
  * face-CFL worked example), Green-Ampt as printed and in the Darcy form (Q15) by SPEC examples and
- * hand-derived capacities, the inflow ghost's discharge (Q18) by the inflow mass rate, icbrt (Q20) by libm
- * cbrt to 2 ulp.  Pinned only by invariants ("parity unpinned" otherwise): the critical-depth height h_c
- * of the inflow ghost (Q18) and the choice V0 = 3 mm (Q15), both problem data rather than arithmetic.
+ * hand-derived capacities, the inflow ghost (Q18) by the inflow mass rate (q) and the closed-form momentum
+ * flux of the critical state (h_c), icbrt (Q20) by libm cbrt to 2 ulp.  No function is left "parity
+ * unpinned"; V0 = 3 mm (Q15) is problem data.
  */
 #ifndef SWOF_ORACLE_H
 #define SWOF_ORACLE_H

@@ -296,3 +296,22 @@ def test_inflow_mass_rate():
     P = oracle.params_from_config(cfg)
     h, _, _, _, _ = oracle.stage(P, cfg.z, None, cfg.h, cfg.hu, cfg.hv, None, 5.0, dt)
     assert abs(h.sum() - 2.0 * dt) <= 1e-13
+
+
+def test_inflow_critical_depth_momentum():
+    """Pins the inflow ghost's critical depth h_c = (q^2/g)^(1/3) (Q18) by its momentum flux: on a dry flat
+    bed the ghost state (h_c, q) is critical (u = sqrt(g h_c)), so the face takes F(U_L) and one stage adds
+    hu = (dt/dx) (q^2/h_c + g h_c^2 / 2) = (dt/dx) 1.5 g h_c^2 to the first cell of every segment row
+    (no slopes, no interface source, zero stage-input velocity -> friction factor 1)."""
+    cfg = flat_cfg(12, 10, bc={"W": "inflow", "E": "wall", "S": "wall", "N": "wall"}, fric_law="manning",
+                   fric_coef=0.03, inflow={"W": Inflow(k0=3, k1=7, hydro_t=[0.0], hydro_q=[2.0])})
+    P = oracle.params_from_config(cfg)
+    dt = 0.01
+    h, hu, hv, _, _ = oracle.stage(P, cfg.z, None, cfg.h, cfg.hu, cfg.hv, None, 0.0, dt)
+    q = 2.0 / 4.0                                        # Q / W, W = 4 cells x dy = 1 m
+    hc = (q * q / G) ** (1.0 / 3.0)
+    want = (dt / cfg.dx) * 1.5 * G * hc * hc
+    for j in range(3, 7):
+        assert abs(hu[j, 0] - want) <= 1e-13 * want, (hu[j, 0], want)
+        assert abs(h[j, 0] - (dt / cfg.dx) * q) <= 1e-16
+    assert np.all(hu[:, 1:] == 0) and np.all(hv == 0)
