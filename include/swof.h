@@ -81,7 +81,7 @@ typedef struct swof_params {
     double g;                /* gravity [m/s^2] (9.81)                                     */
     double cfl;              /* n_CFL in (0, 1]                                          */
     double dt_max;           /* [s] > 0; also the step of an all-dry domain                      */
-    double h_eps;            /* dry threshold [m] >= 0: wet <=> h > h_eps                         */
+    double h_eps;            /* dry threshold [m] >= 1e-300: wet <=> h > h_eps                    */
     int32_t fric_law;        /* SWOF_FRIC_*                                                      */
     double fric_coef;        /* n, K, f or C (> 0 unless NONE); ignored when a per-cell field is given */
     int32_t ga_enabled;      /* Green-Ampt                                           */

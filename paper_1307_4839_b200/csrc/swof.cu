@@ -80,7 +80,8 @@ const char* validate(const swof_params* p) {
     if (!(p->g > 0) || !std::isfinite(p->g)) return "g must be > 0";
     if (!(p->cfl > 0) || p->cfl > 1) return "cfl must be in (0, 1]";
     if (!(p->dt_max > 0) || !std::isfinite(p->dt_max)) return "dt_max must be finite and > 0";
-    if (!(p->h_eps >= 0) || !std::isfinite(p->h_eps)) return "h_eps must be finite and >= 0";
+    // the kernels' fast reciprocal of wet depths needs h > h_eps >= 2^-1000 (1e-300 is 0 for any physics)
+    if (!(p->h_eps >= 1e-300) || !std::isfinite(p->h_eps)) return "h_eps must be finite and >= 1e-300";
     if (p->fric_law < SWOF_FRIC_NONE || p->fric_law > SWOF_FRIC_CHEZY) return "unknown fric_law";
     if (p->ga_enabled) {
         if (!(p->ga_Ks >= 0) || !(p->ga_dtheta > 0) || !std::isfinite(p->ga_hf) || !std::isfinite(p->ga_A) ||
