@@ -16,6 +16,12 @@
 #include "../../include/swof.h"
 #include "swof_kernels.cuh"
 #include "swof_d8.cuh"
+#ifndef SWOF_MARCH
+#define SWOF_MARCH 1                   // 1: the register-marching stage kernel (swof_march.cuh) by default
+#endif
+#if SWOF_MARCH
+#include "swof_march.cuh"
+#endif
 
 using namespace swof;
 
@@ -37,6 +43,8 @@ struct swof_ctx {
     dim3 grid;
     StageFn kpred = nullptr, kcorr = nullptr;   // stage kernel instances for this context's physics
     dim3 cf_grid;                               // face-CFL pass tiles
+    dim3 sgrid, sblock;                         // stage kernel launch shape
+    size_t ssmem = 0;
     std::string err;
 };
 
@@ -141,11 +149,11 @@ constexpr int PW_BLOCKS = 1184;        // point-wise / face-CFL passes: 8 CTAs x
 // (explicit Euler), then the reconstructed-value CFL pass when SWOF_CFL_FACE
 void launch_second(swof_ctx* c, int par, cudaStream_t s) {
     if (c->kp.order == 1) euler_commit_kernel<<<PW_BLOCKS, PW_NT, 0, s>>>(c->kp, c->kb, par);
-    else c->kcorr<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
+    else c->kcorr<<<c->sgrid, c->sblock, c->ssmem, s>>>(c->kp, c->kb, par);
     if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<c->cf_grid, dim3(CF_TX, CF_NTY), 0, s>>>(c->kp, c->kb, par, 0);
 }
 void launch_step(swof_ctx* c, int par, cudaStream_t s) {
-    c->kpred<<<c->grid, NT, SMEM_BYTES, s>>>(c->kp, c->kb, par);
+    c->kpred<<<c->sgrid, c->sblock, c->ssmem, s>>>(c->kp, c->kb, par);
     launch_second(c, par, s);
 }
 void launch_step(swof_ctx* c, int par) { launch_step(c, par, c->stream); }
@@ -267,6 +275,40 @@ int swof_workspace_size(const swof_params* p, size_t* bytes) {
     return SWOF_OK;
 }
 
+// Picks the stage kernels for the context's physics and options and their launch shape: the marching
+// kernel (swof_march.cuh) by default; the tiled stage_kernel for the fused halo push and the dry-tile skip.
+static int choose_kernels(swof_ctx* c) {
+    const KParams& k = c->kp;
+    const bool ff = c->kb.fric != nullptr;
+    const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
+    const bool push = c->kb.push_any != 0, dry = c->p.dry_skip != 0;
+#if SWOF_MARCH
+    if (!push && !dry) {
+        c->kpred = select_march<false>(k.fk, k.ga != 0, ff, generic);
+        c->kcorr = select_march<true>(k.fk, k.ga != 0, ff, generic);
+        // rows per warp: 64 (2 halo rows of slopes and faces per 64; a wave model chasing the tail of the
+        // last wave measured no better)
+        const char* fixed = getenv("SWOF_MARCH_H");
+        const int mh = fixed && atoi(fixed) > 0 ? atoi(fixed) : 64;
+        c->kp.march_h = mh;
+        const long long nwarps = (long long)((k.nx + M_OWN - 1) / M_OWN) * ((k.ny + mh - 1) / mh);
+        c->sgrid = dim3((unsigned)((nwarps + M_NW - 1) / M_NW));
+        c->sblock = dim3(M_NW * 32);
+        c->ssmem = 0;
+        return SWOF_OK;
+    }
+#endif
+    c->kpred = select_stage<false>(k.fk, k.ga != 0, ff, generic, push, dry);
+    c->kcorr = select_stage<true>(k.fk, k.ga != 0, ff, generic, push, dry);
+    cudaError_t e = cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(c, e, "stage kernel attributes");
+    c->sgrid = c->grid;
+    c->sblock = dim3(NT);
+    c->ssmem = SMEM_BYTES;
+    return SWOF_OK;
+}
+
 int swof_create(const swof_params* p, const double* z, const double* fric_field, void* d_workspace, size_t ws_bytes,
                 void* cuda_stream, swof_ctx** out) {
     if (!out) return SWOF_EINVAL;
@@ -336,14 +378,14 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     c->diag_blocks = DIAG_BLOCKS;
     c->cf_grid = dim3((unsigned)((p->nx + CF_TX - 1) / CF_TX), (unsigned)((p->ny + CF_TY - 1) / CF_TY));
 
-    const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
-    c->kpred = select_stage<false>(k.fk, k.ga != 0, has_ff, generic, false, p->dry_skip != 0);
-    c->kcorr = select_stage<true>(k.fk, k.ga != 0, has_ff, generic, false, p->dry_skip != 0);
-    cudaError_t e = cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    {   // resident CTAs of the stage kernel: the distance of the next-tile L2 prefetch
+    {
+        const int rc = choose_kernels(c);
+        if (rc != SWOF_OK) { swof_destroy(c); return rc; }
+    }
+    cudaError_t e = cudaSuccess;
+    {   // resident CTAs of the tiled stage kernel: the distance of its (off by default) next-tile L2 prefetch
         int per_sm = 0, dev = 0, sms = 0;
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kpred, NT, SMEM_BYTES);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_stage<false>(k.fk, k.ga != 0, has_ff, true, false, false), NT, SMEM_BYTES);
         if (e == cudaSuccess) e = cudaGetDevice(&dev);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         k.pf_stride = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 1);
@@ -521,7 +563,7 @@ int swof_predictor(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf
     int rc;
     if ((rc = read_state(c))) return rc;
     saved = *c->h_st;
-    c->kpred<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+    c->kpred<<<c->sgrid, c->sblock, c->ssmem, c->stream>>>(c->kp, c->kb, c->par);
     CK(cudaGetLastError());
     if (h && (rc = copy_field_out(c, h, c->kb.Bh))) return rc;
     if (hu && (rc = copy_field_out(c, hu, c->kb.Bhu))) return rc;
@@ -545,7 +587,7 @@ int swof_step_profiled(swof_ctx* c, int64_t nsteps, double* ms) {
     double acc[2] = {0, 0};
     for (int64_t n = 0; n < nsteps; ++n) {
         CK(cudaEventRecord(ev[0], c->stream));
-        c->kpred<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+        c->kpred<<<c->sgrid, c->sblock, c->ssmem, c->stream>>>(c->kp, c->kb, c->par);
         CK(cudaEventRecord(ev[1], c->stream));
         launch_second(c, c->par, c->stream);
         CK(cudaEventRecord(ev[2], c->stream));
@@ -599,14 +641,9 @@ int swof_set_halo_push(swof_ctx* c, int32_t side, double* const* set0, double* c
     c->kb.push_any = 0;
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) c->kb.push_any |= c->kb.push[a][b][0] != nullptr;
-    // the pushing kernels are the generic instance compiled with the fused exchange
-    const bool generic = c->kp.flux != SWOF_FLUX_HLL || c->kp.order == 1 || c->kp.ga_form != SWOF_GA_PRINTED;
-    c->kpred = select_stage<false>(c->kp.fk, c->kp.ga != 0, c->kb.fric != nullptr, generic, c->kb.push_any != 0,
-                                   c->p.dry_skip != 0);
-    c->kcorr = select_stage<true>(c->kp.fk, c->kp.ga != 0, c->kb.fric != nullptr, generic, c->kb.push_any != 0,
-                                  c->p.dry_skip != 0);
-    CK(cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-    CK(cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    // the pushing kernels are the generic tiled instance compiled with the fused exchange
+    const int rc = choose_kernels(c);
+    if (rc != SWOF_OK) return rc;
     if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }   // kernels changed
     return SWOF_OK;
 }
@@ -645,10 +682,10 @@ int swof_enqueue_phase(swof_ctx* c, int32_t phase) {
     if (!c) return SWOF_EINVAL;
     if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_enqueue_phase before swof_set_state");
     if (phase == 0) {
-        c->kpred<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+        c->kpred<<<c->sgrid, c->sblock, c->ssmem, c->stream>>>(c->kp, c->kb, c->par);
     } else if (phase == 1) {
         if (c->kp.order == 1) euler_commit_kernel<<<PW_BLOCKS, PW_NT, 0, c->stream>>>(c->kp, c->kb, c->par);
-        else c->kcorr<<<c->grid, NT, SMEM_BYTES, c->stream>>>(c->kp, c->kb, c->par);
+        else c->kcorr<<<c->sgrid, c->sblock, c->ssmem, c->stream>>>(c->kp, c->kb, c->par);
     } else if (phase == 2) {
         if (c->kp.cfl_mode == SWOF_CFL_FACE) cfl_face_kernel<<<c->cf_grid, dim3(CF_TX, CF_NTY), 0, c->stream>>>(c->kp, c->kb, c->par, 0);
         c->par ^= 1;                          // the step is complete

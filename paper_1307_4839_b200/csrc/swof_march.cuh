@@ -1,0 +1,318 @@
+// swof_march.cuh -- an alternative stage kernel that keeps the stencil in registers: each warp owns a
+// strip of 28 columns (lanes 2..29 of the 32 columns i0-2 .. i0+29) and marches down MH rows.  The
+// y-direction (slopes, reconstruction, faces) lives in a 3-row register window, the x-direction goes
+// through warp shuffles (neighbour primitives, the left cell's high face, the east face's flux), so there
+// is no shared-memory tile and no CTA barrier in the stencil.  Same arithmetic as stage_kernel (the
+// canonical sheet of DESIGN.md §3), hence the same bits.  The default stage kernel (SWOF_MARCH=1); the tiled
+// stage_kernel stays for the fused halo push and the dry-tile skip.
+#pragma once
+
+namespace swof {
+
+constexpr int M_OWN = 28;              // own columns per warp
+#ifndef SWOF_MARCH_NW
+#define SWOF_MARCH_NW 4
+#endif
+constexpr int M_NW = SWOF_MARCH_NW;    // warps per CTA (independent); rows per warp: KParams::march_h
+#ifndef SWOF_MARCH_MINB
+#define SWOF_MARCH_MINB 4
+#endif
+
+struct MPrim { double h, e, u, v, rh; };
+
+__device__ __forceinline__ double2 shup2(double2 v) {
+    return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ double2 shdn2(double2 v) {
+    return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ double shup(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+// (h, hu, hv, z) of cell (gi, gj) with the boundary ghosts of stage_kernel's edge path; any cell
+// outside in both directions (a corner, never used) returns zeros
+__device__ __forceinline__ void march_fetch(const KParams& P, const KBufs& B, const double* in_h, const double* in_hu,
+                                            const double* in_hv, const Ghost* G, int gx, int gy, double& h,
+                                            double& hu, double& hv, double& z) {
+    const int nx = P.nx, ny = P.ny;
+    const bool xin = gx >= 0 && gx < nx, yin = gy >= 0 && gy < ny;
+    if (xin && yin) {
+        const size_t o = (size_t)gy * P.pitch + gx;
+        h = in_h[o];
+        hu = in_hu[o];
+        hv = in_hv[o];
+        z = B.z[o];
+        return;
+    }
+    h = hu = hv = z = 0.0;
+    if (!xin && !yin) return;
+    int si = gx, sj = gy, side;
+    bool fx = false, fy = false, inflow = false;
+    if (!xin) {
+        side = gx < 0 ? 0 : 1;
+        const bool inseg = P.bc[side] == BC_INFLOW && gy >= P.k0[side] && gy < P.k1[side];
+        si = bc_src(gx, nx, P.bc[0], P.bc[1], inseg, inseg, fx);
+        inflow = inseg;
+    } else {
+        side = gy < 0 ? 2 : 3;
+        const bool inseg = P.bc[side] == BC_INFLOW && gx >= P.k0[side] && gx < P.k1[side];
+        sj = P.bc[side] == BC_HALO ? (gy < -GHOST_ROWS ? -GHOST_ROWS : gy >= ny + GHOST_ROWS ? ny + GHOST_ROWS - 1 : gy)
+                                   : bc_src(gy, ny, P.bc[2], P.bc[3], inseg, inseg, fy);
+        inflow = inseg;
+    }
+    const size_t o = (size_t)sj * P.pitch + si;
+    z = B.z[o];
+    if (inflow) {  // G in shared memory (one copy per CTA)
+        h = G->hc[side];
+        hu = side == 0 ? G->q[0] : (side == 1 ? -G->q[1] : 0.0);
+        hv = side == 2 ? G->q[2] : (side == 3 ? -G->q[3] : 0.0);
+    } else {
+        h = in_h[o];
+        hu = in_hu[o];
+        hv = in_hv[o];
+        if (fx) hu = -hu;
+        if (fy) hv = -hv;
+    }
+}
+
+template <bool CORRECTOR, class PH>
+__global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const KParams P, const KBufs B, const int par) {
+    __shared__ double s_sc[6];
+    __shared__ Ghost s_g;
+    __shared__ int s_done;
+    DevState* st = B.st;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool leader = blockIdx.x == 0 && tid == 0;
+    if (tid == 0) {
+        const double t = st->t[par];
+        const long long step = st->step[par];
+        const double ax = u2d(st->amax[par][0]), ay = u2d(st->amax[par][1]);
+        const double t_end = st->t_end;
+        const bool finite = isfinite(ax) && isfinite(ay);
+        const bool done = !(t < t_end) || step >= st->step_limit || !finite;
+        if (leader) {
+            if (done) {
+                if (!CORRECTOR) {
+                    st->amax[par ^ 1][0] = st->amax[par][0];
+                    st->amax[par ^ 1][1] = st->amax[par][1];
+                    if (!finite) atomicOr(&st->flags, FLAG_NONFINITE);
+                } else {
+                    st->t[par ^ 1] = t;
+                    st->step[par ^ 1] = step;
+                }
+            } else if (!CORRECTOR) {
+                st->amax[par ^ 1][0] = 0ull;
+                st->amax[par ^ 1][1] = 0ull;
+            }
+        }
+        const double dt0 = cfl_dt(P, ax, ay, t, t_end);
+        const double ts0 = CORRECTOR ? t + dt0 : t;
+        s_done = done;
+        s_sc[0] = dt0;
+        s_sc[1] = ts0;
+        s_sc[2] = dt0 / P.dx;
+        s_sc[3] = dt0 / P.dy;
+        s_sc[4] = rain_rate(P, ts0) * dt0;
+        s_sc[5] = (ph_ff<PH>(P) || ph_fk<PH>(P) == 0) ? 0.0 : dt0 * friction_gcf(P.fric_law, P.fric_coef, P.g);
+        for (int k = 0; k < 4; ++k) {
+            s_g.q[k] = 0.0;
+            s_g.hc[k] = 0.0;
+            if (P.bc[k] == BC_INFLOW) {
+                s_g.q[k] = hydrograph(P, k, ts0) / P.width[k];
+                s_g.hc[k] = critical_depth(s_g.q[k], P.g);
+            }
+        }
+    }
+    __syncthreads();
+    if (s_done) return;
+    const double dt = s_sc[0], lx = s_sc[2], ly = s_sc[3], Rdt = s_sc[4], dtgcf0 = s_sc[5];
+    const int nx = P.nx, ny = P.ny, pitch = P.pitch;
+    const int nstrip = (nx + M_OWN - 1) / M_OWN;
+    const int wid = blockIdx.x * M_NW + warp;
+    const int s = wid % nstrip, g = wid / nstrip;
+    const int i0 = s * M_OWN, j0 = g * P.march_h;
+    double amx = 0.0, amy = 0.0;
+    if (j0 < ny) {
+        const double* __restrict__ in_h = CORRECTOR ? B.Bh : B.Ah;
+        const double* __restrict__ in_hu = CORRECTOR ? B.Bhu : B.Ahu;
+        const double* __restrict__ in_hv = CORRECTOR ? B.Bhv : B.Ahv;
+        const double h_eps = P.h_eps, g2 = 0.5 * P.g;
+        const bool rus = ph_rusanov<PH>(P);              // Rusanov flux (generic instance only)
+        const bool ord1 = ph_order1<PH>(P);              // first order: every slope is 0
+        const double2 z2 = make_double2(0.0, 0.0);
+        const int gi = i0 - HALO + lane;
+        const bool own_col = lane >= HALO && lane < HALO + M_OWN && gi < nx;
+        const int jend = j0 + P.march_h < ny ? j0 + P.march_h : ny;
+        auto prim = [&](double h, double hu, double hv, double z, MPrim& m) {
+            const double rh = (h > h_eps) ? drcp(h) : 0.0;
+            m.h = h;
+            m.e = h + z;
+            m.u = hu * rh;
+            m.v = hv * rh;
+            m.rh = rh;
+        };
+        // window: A = row j-2, Bw = row j-1, C = row j
+        MPrim A, Bw, C;
+        double rh_, rhu, rhv, rz;                     // raw (h, hu, hv, z) of row j, fetched one row ahead
+        march_fetch(P, B, in_h, in_hu, in_hv, &s_g, gi, j0 - 2, rh_, rhu, rhv, rz);
+        prim(rh_, rhu, rhv, rz, A);
+        march_fetch(P, B, in_h, in_hu, in_hv, &s_g, gi, j0 - 1, rh_, rhu, rhv, rz);
+        prim(rh_, rhu, rhv, rz, Bw);
+        march_fetch(P, B, in_h, in_hu, in_hv, &s_g, gi, j0, rh_, rhu, rhv, rz);
+        // carried from the previous row: the high y face of row j-2 (for the face between j-2 and j-1), the
+        // south face flux of row j-2 (Fm, Fn + S_R, Ft) and its y slopes {dh, de} (Fc_y)
+        FaceIn plusA;
+        double2 sfa = make_double2(0.0, 0.0), sfb = make_double2(0.0, 0.0), slA = make_double2(0.0, 0.0);
+        plusA.h = plusA.e = plusA.z = plusA.n = plusA.t = 0.0;
+        for (int j = j0; j <= jend + 1; ++j) {
+            prim(rh_, rhu, rhv, rz, C);
+            if (j <= jend) march_fetch(P, B, in_h, in_hu, in_hv, &s_g, gi, j + 1, rh_, rhu, rhv, rz);
+            // the finalised row's own state, issued early
+            const int f = j - 2;
+            const bool own = own_col && f >= j0;
+            const size_t o = (size_t)(own ? f : 0) * pitch + (own ? gi : 0);
+            double hus = 0.0, hvs = 0.0, V = 0.0, cf = P.fric_coef, Ah0 = 0.0, Ahu0 = 0.0, Ahv0 = 0.0, VA0 = 0.0;
+            if (own) {
+                hus = in_hu[o];
+                hvs = in_hv[o];
+                if (ph_ga<PH>(P)) V = CORRECTOR ? B.VB[o] : B.VA[o];
+                if (ph_ff<PH>(P)) cf = B.fric[o];
+                if (CORRECTOR) {
+                    Ah0 = B.Ah[o];
+                    Ahu0 = B.Ahu[o];
+                    Ahv0 = B.Ahv[o];
+                    if (ph_ga<PH>(P)) VA0 = B.VA[o];
+                }
+            }
+            // y slopes and y reconstruction of row m = j-1 (normal v, transverse u)
+            const double2 saB = ord1 ? z2 : half_slopes(A.h, Bw.h, C.h, A.e, Bw.e, C.e);
+            const double2 sbB = ord1 ? z2 : half_slopes(A.v, Bw.v, C.v, A.u, Bw.u, C.u);
+            const FaceIn minusB = recon_minus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
+            const FaceIn plusB = recon_plus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
+            if (j - 1 >= j0) {
+                // y face between rows j-2 and j-1: the north face of row j-2, the south face of row j-1
+                double2 nfa, nfb;
+                if (face_flux<false>(P.g, h_eps, plusA, minusB, nfa, nfb, rus))
+                    face_flux<true>(P.g, h_eps, plusA, minusB, nfa, nfb, rus);
+                if (j - 2 >= j0) {
+                    // ---- finalise row f = j-2 (window A): x direction by shuffles, update, sources ----
+                    const double2 heA = make_double2(A.h, A.e);
+                    const double2 cL = shup2(heA), cR = shdn2(heA);
+                    const double2 uvA = make_double2(A.u, A.v);
+                    const double2 uL = shup2(uvA), uR = shdn2(uvA);
+                    const double2 sa = ord1 ? z2 : half_slopes(cL.x, A.h, cR.x, cL.y, A.e, cR.y);
+                    const double2 sb = ord1 ? z2 : half_slopes(uL.x, A.u, uR.x, uL.y, A.v, uR.y);
+                    const FaceIn pl = recon_plus(heA, A.u, A.v, A.rh, sa, sb);
+                    const FaceIn mi = recon_minus(heA, A.u, A.v, A.rh, sa, sb);
+                    FaceIn lp;                                // the west neighbour's high face
+                    lp.h = shup(pl.h);
+                    lp.e = shup(pl.e);
+                    lp.z = shup(pl.z);
+                    lp.n = shup(pl.n);
+                    lp.t = shup(pl.t);
+                    double2 wa, wb;                           // west face of this lane's cell
+                    if (face_flux<false>(P.g, h_eps, lp, mi, wa, wb, rus)) face_flux<true>(P.g, h_eps, lp, mi, wa, wb, rus);
+                    const double2 ea = shdn2(wa), eb = shdn2(wb);
+                    const double Fcx = centred_source(g2, A.h, A.e, sa.x, sa.y);
+                    const double pxm = lx * (ea.x - wa.x);
+                    const double qx = lx * ((ea.y - wb.x) - Fcx), qy = lx * (eb.y - wb.y);
+                    // y half with the south (carried) and north (just computed) faces
+                    const double Fcy = centred_source(g2, A.h, A.e, slA.x, slA.y);
+                    const double Dm = nfa.x - sfa.x;
+                    const double Dn = (nfa.y - sfb.x) - Fcy;
+                    const double Dt = nfb.y - sfb.y;
+                    const double hh = A.h - (pxm + ly * Dm);
+                    const double hu1 = hus - (qx + ly * Dt);
+                    const double hv1 = hvs - (qy + ly * Dn);
+                    const double cl = (own && hh < 0.0) ? -hh : 0.0;
+                    const double h1 = hh < 0.0 ? 0.0 : hh;
+                    double hst, hu2, hv2, Vn;
+                    if (cell_sources<PH, false>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn))
+                        cell_sources<PH, true>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn);
+                    if (cl > 0.0) {
+                        atomicAdd(&st->clamps, 1ull);
+                        atomicAdd(&st->clamped_mass, cl);
+                        if (atomicMax(&st->clamp_max_bits, d2u(cl)) < d2u(cl)) {
+                            atomicExch((unsigned long long*)&st->big_clamp_cell, (unsigned long long)((long long)f * nx + gi));
+                            atomicExch((unsigned long long*)&st->big_clamp_step, (unsigned long long)st->step[par]);
+                        }
+                        if (cl > P.clamp_fail) atomicOr(&st->flags, FLAG_BIGCLAMP);
+                    }
+                    if (own) {
+                        if (!CORRECTOR) {
+                            B.Bh[o] = hst;
+                            B.Bhu[o] = hu2;
+                            B.Bhv[o] = hv2;
+                            if (ph_ga<PH>(P)) B.VB[o] = Vn;
+                        } else {
+                            const double hN = 0.5 * (Ah0 + hst);
+                            const double huN = 0.5 * (Ahu0 + hu2);
+                            const double hvN = 0.5 * (Ahv0 + hv2);
+                            B.Ah[o] = hN;
+                            B.Ahu[o] = huN;
+                            B.Ahv[o] = hvN;
+                            if (ph_ga<PH>(P)) B.VA[o] = 0.5 * (VA0 + Vn);
+                            if (P.cfl_mode == 0) {
+                                double su, sv;
+                                if (cfl_speeds<false>(P, hN, huN, hvN, su, sv)) cfl_speeds<true>(P, hN, huN, hvN, su, sv);
+                                amx = (su > amx || su != su) ? su : amx;
+                                amy = (sv > amy || sv != sv) ? sv : amy;
+                            }
+                        }
+                    }
+                }
+                sfa = make_double2(nfa.x, nfa.y);              // becomes the south face of row j-1
+                sfb = nfb;
+            }
+            // slide the window
+            plusA = plusB;
+            slA = saB;
+            A = Bw;
+            Bw = C;
+        }
+    }
+    if (CORRECTOR) {
+        __shared__ unsigned long long red[2][M_NW];
+        unsigned long long bx = d2u(amx), by = d2u(amy);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long ox = __shfl_xor_sync(0xffffffffu, bx, off);
+            const unsigned long long oy = __shfl_xor_sync(0xffffffffu, by, off);
+            bx = ox > bx ? ox : bx;
+            by = oy > by ? oy : by;
+        }
+        if (lane == 0) { red[0][warp] = bx; red[1][warp] = by; }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long mx = 0, my = 0;
+            for (int w = 0; w < M_NW; ++w) {
+                mx = red[0][w] > mx ? red[0][w] : mx;
+                my = red[1][w] > my ? red[1][w] : my;
+            }
+            atomicMax(&st->amax[par ^ 1][0], mx);
+            atomicMax(&st->amax[par ^ 1][1], my);
+            if (leader) {
+                const double tn = st->t[par];
+                const long long n = st->step[par];
+                st->t[par ^ 1] = tn + dt;
+                st->step[par ^ 1] = n + 1;
+                if (n < B.dt_cap) B.dt_hist[n] = dt;
+            }
+        }
+    }
+}
+
+template <bool C, int FK, bool GA, bool FF>
+constexpr StageFn march_fn() { return march_kernel<C, Phys<FK, GA, FF>>; }
+template <bool C>
+__host__ inline StageFn select_march(int fk, bool ga, bool ff, bool generic) {
+    if (generic) return march_kernel<C, PhysRT>;
+    static const StageFn tab[3][2][2] = {
+        {{march_fn<C, 0, false, false>(), march_fn<C, 0, false, true>()}, {march_fn<C, 0, true, false>(), march_fn<C, 0, true, true>()}},
+        {{march_fn<C, 1, false, false>(), march_fn<C, 1, false, true>()}, {march_fn<C, 1, true, false>(), march_fn<C, 1, true, true>()}},
+        {{march_fn<C, 2, false, false>(), march_fn<C, 2, false, true>()}, {march_fn<C, 2, true, false>(), march_fn<C, 2, true, true>()}},
+    };
+    return tab[fk][ga][ff];
+}
+
+}  // namespace swof
