@@ -10,12 +10,15 @@
 namespace swof {
 
 constexpr int M_OWN = 28;              // own columns per warp
+#ifndef SWOF_MARCH_UNROLL
+#define SWOF_MARCH_UNROLL 1
+#endif
 #ifndef SWOF_MARCH_NW
 #define SWOF_MARCH_NW 4
 #endif
 constexpr int M_NW = SWOF_MARCH_NW;    // warps per CTA (independent); rows per warp: KParams::march_h
 #ifndef SWOF_MARCH_MINB
-#define SWOF_MARCH_MINB 4
+#define SWOF_MARCH_MINB 3
 #endif
 
 struct MPrim { double h, e, u, v, rh; };
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         const int gi = i0 - HALO + lane;
         const bool own_col = lane >= HALO && lane < HALO + M_OWN && gi < nx;
         const int jend = j0 + P.march_h < ny ? j0 + P.march_h : ny;
+        const bool fastx = i0 - HALO >= 0 && i0 - HALO + 32 <= nx;   // all 32 columns inside (warp-uniform)
         auto prim = [&](double h, double hu, double hv, double z, MPrim& m) {
             const double rh = (h > h_eps) ? drcp(h) : 0.0;
             m.h = h;
@@ -164,25 +168,36 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         FaceIn plusA;
         double2 sfa = make_double2(0.0, 0.0), sfb = make_double2(0.0, 0.0), slA = make_double2(0.0, 0.0);
         plusA.h = plusA.e = plusA.z = plusA.n = plusA.t = 0.0;
+_Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
         for (int j = j0; j <= jend + 1; ++j) {
             prim(rh_, rhu, rhv, rz, C);
-            if (j <= jend) march_fetch(P, B, in_h, in_hu, in_hv, &s_g, gi, j + 1, rh_, rhu, rhv, rz);
-            // the finalised row's own state, issued early
+            if (j <= jend) {
+                const int jn = j + 1;
+                if (fastx && jn < ny) {
+                    const size_t on = (size_t)jn * pitch + gi;
+                    rh_ = in_h[on];
+                    rhu = in_hu[on];
+                    rhv = in_hv[on];
+                    rz = B.z[on];
+                } else {
+                    march_fetch(P, B, in_h, in_hu, in_hv, &s_g, gi, jn, rh_, rhu, rhv, rz);
+                }
+            }
+            // the finalised row's own state, issued early; unconditional loads (a non-own lane reads cell
+            // (0, 0), always allocated) keep the loop free of divergent branches
             const int f = j - 2;
             const bool own = own_col && f >= j0;
             const size_t o = (size_t)(own ? f : 0) * pitch + (own ? gi : 0);
-            double hus = 0.0, hvs = 0.0, V = 0.0, cf = P.fric_coef, Ah0 = 0.0, Ahu0 = 0.0, Ahv0 = 0.0, VA0 = 0.0;
-            if (own) {
-                hus = in_hu[o];
-                hvs = in_hv[o];
-                if (ph_ga<PH>(P)) V = CORRECTOR ? B.VB[o] : B.VA[o];
-                if (ph_ff<PH>(P)) cf = B.fric[o];
-                if (CORRECTOR) {
-                    Ah0 = B.Ah[o];
-                    Ahu0 = B.Ahu[o];
-                    Ahv0 = B.Ahv[o];
-                    if (ph_ga<PH>(P)) VA0 = B.VA[o];
-                }
+            double V = 0.0, cf = P.fric_coef, Ah0 = 0.0, Ahu0 = 0.0, Ahv0 = 0.0, VA0 = 0.0;
+            const double hus = in_hu[o];
+            const double hvs = in_hv[o];
+            if (ph_ga<PH>(P)) V = CORRECTOR ? B.VB[o] : B.VA[o];
+            if (ph_ff<PH>(P)) cf = B.fric[o];
+            if (CORRECTOR) {
+                Ah0 = B.Ah[o];
+                Ahu0 = B.Ahu[o];
+                Ahv0 = B.Ahv[o];
+                if (ph_ga<PH>(P)) VA0 = B.VA[o];
             }
             // y slopes and y reconstruction of row m = j-1 (normal v, transverse u)
             const double2 saB = ord1 ? z2 : half_slopes(A.h, Bw.h, C.h, A.e, Bw.e, C.e);
