@@ -314,7 +314,7 @@ def main():
             with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
                 prof = json.load(f)
             for kname, k in prof["kernels"].items():
-                is_corr = re.search(r"stage_kernel<(\(bool\))?(1|true)\b", kname) is not None
+                is_corr = re.search(r"(stage|march)_kernel<(\(bool\))?(1|true)\b", kname) is not None
                 if is_corr == (dom == "corrector"):
                     traffic = k["dram_bytes_per_cell"] * cells
                     tsrc = f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"

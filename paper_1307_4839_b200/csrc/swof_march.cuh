@@ -13,6 +13,22 @@ constexpr int M_OWN = 28;              // own columns per warp
 #ifndef SWOF_MARCH_UNROLL
 #define SWOF_MARCH_UNROLL 1
 #endif
+// the rare exact recomputation (SLOW) of an out-of-range lane: per lane (divergent), or, with
+// SWOF_MARCH_VOTE, by the whole warp when any lane needs it (a uniform branch; SLOW gives the same bits)
+#ifndef SWOF_MARCH_VOTE
+#define SWOF_MARCH_VOTE 1
+#endif
+#if SWOF_MARCH_VOTE
+#define M_SLOW(...) __any_sync(0xffffffffu, (__VA_ARGS__))
+#else
+#define M_SLOW(...) (__VA_ARGS__)
+#endif
+#ifndef SWOF_MARCH_UNCOND
+#define SWOF_MARCH_UNCOND 0
+#endif
+#ifndef SWOF_MARCH_SCV
+#define SWOF_MARCH_SCV 0
+#endif
 #ifndef SWOF_MARCH_NW
 #define SWOF_MARCH_NW 4
 #endif
@@ -63,6 +79,7 @@ __device__ __forceinline__ void march_fetch(const KParams& P, const KBufs& B, co
                                    : bc_src(gy, ny, P.bc[2], P.bc[3], inseg, inseg, fy);
         inflow = inseg;
     }
+    SWOF_ASSERT(si >= 0 && si < nx && sj >= -GHOST_ROWS && sj < ny + GHOST_ROWS);
     const size_t o = (size_t)sj * P.pitch + si;
     z = B.z[o];
     if (inflow) {  // G in shared memory (one copy per CTA)
@@ -128,7 +145,11 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
     }
     __syncthreads();
     if (s_done) return;
+#if SWOF_MARCH_SCV    // re-read the step scalars from shared memory at each use (register pressure experiment)
+    const volatile double &dt = s_sc[0], &lx = s_sc[2], &ly = s_sc[3], &Rdt = s_sc[4], &dtgcf0 = s_sc[5];
+#else
     const double dt = s_sc[0], lx = s_sc[2], ly = s_sc[3], Rdt = s_sc[4], dtgcf0 = s_sc[5];
+#endif
     const int nx = P.nx, ny = P.ny, pitch = P.pitch;
     const int nstrip = (nx + M_OWN - 1) / M_OWN;
     const int wid = blockIdx.x * M_NW + warp;
@@ -175,6 +196,7 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                 const int jn = j + 1;
                 if (fastx && jn < ny) {
                     const size_t on = (size_t)jn * pitch + gi;
+                    SWOF_ASSERT(jn >= 0 && jn < ny && gi >= 0 && gi < nx);
                     rh_ = in_h[on];
                     rhu = in_hu[on];
                     rhv = in_hv[on];
@@ -188,6 +210,7 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
             const int f = j - 2;
             const bool own = own_col && f >= j0;
             const size_t o = (size_t)(own ? f : 0) * pitch + (own ? gi : 0);
+            SWOF_ASSERT(!own || (f >= 0 && f < ny && gi >= 0 && gi < nx));
             double V = 0.0, cf = P.fric_coef, Ah0 = 0.0, Ahu0 = 0.0, Ahv0 = 0.0, VA0 = 0.0;
             const double hus = in_hu[o];
             const double hvs = in_hv[o];
@@ -204,12 +227,20 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
             const double2 sbB = ord1 ? z2 : half_slopes(A.v, Bw.v, C.v, A.u, Bw.u, C.u);
             const FaceIn minusB = recon_minus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
             const FaceIn plusB = recon_plus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
+#if SWOF_MARCH_UNCOND
+            {   // computed from j0 on (the first two rows' results are discarded): one straight loop body
+#else
             if (j - 1 >= j0) {
+#endif
                 // y face between rows j-2 and j-1: the north face of row j-2, the south face of row j-1
                 double2 nfa, nfb;
-                if (face_flux<false>(P.g, h_eps, plusA, minusB, nfa, nfb, rus))
+                if (M_SLOW(face_flux<false>(P.g, h_eps, plusA, minusB, nfa, nfb, rus)))
                     face_flux<true>(P.g, h_eps, plusA, minusB, nfa, nfb, rus);
+#if SWOF_MARCH_UNCOND
+                {
+#else
                 if (j - 2 >= j0) {
+#endif
                     // ---- finalise row f = j-2 (window A): x direction by shuffles, update, sources ----
                     const double2 heA = make_double2(A.h, A.e);
                     const double2 cL = shup2(heA), cR = shdn2(heA);
@@ -226,7 +257,7 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                     lp.n = shup(pl.n);
                     lp.t = shup(pl.t);
                     double2 wa, wb;                           // west face of this lane's cell
-                    if (face_flux<false>(P.g, h_eps, lp, mi, wa, wb, rus)) face_flux<true>(P.g, h_eps, lp, mi, wa, wb, rus);
+                    if (M_SLOW(face_flux<false>(P.g, h_eps, lp, mi, wa, wb, rus))) face_flux<true>(P.g, h_eps, lp, mi, wa, wb, rus);
                     const double2 ea = shdn2(wa), eb = shdn2(wb);
                     const double Fcx = centred_source(g2, A.h, A.e, sa.x, sa.y);
                     const double pxm = lx * (ea.x - wa.x);
@@ -242,7 +273,7 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                     const double cl = (own && hh < 0.0) ? -hh : 0.0;
                     const double h1 = hh < 0.0 ? 0.0 : hh;
                     double hst, hu2, hv2, Vn;
-                    if (cell_sources<PH, false>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn))
+                    if (M_SLOW(cell_sources<PH, false>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn)))
                         cell_sources<PH, true>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn);
                     if (cl > 0.0) {
                         atomicAdd(&st->clamps, 1ull);
@@ -267,7 +298,7 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                             B.Ahu[o] = huN;
                             B.Ahv[o] = hvN;
                             if (ph_ga<PH>(P)) B.VA[o] = 0.5 * (VA0 + Vn);
-                            if (P.cfl_mode == 0) {
+                            if (P.cfl_mode == 0) {   // own lanes only (divergent: no warp vote here)
                                 double su, sv;
                                 if (cfl_speeds<false>(P, hN, huN, hvN, su, sv)) cfl_speeds<true>(P, hN, huN, hvN, su, sv);
                                 amx = (su > amx || su != su) ? su : amx;

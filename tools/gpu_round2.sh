@@ -7,5 +7,5 @@ timeout 900 python bench.py --steps 50 --warmup 5 > gpurun_out/bench.log 2>&1; e
 CMD="python bench.py --nx 4096 --ny 4096 --steps 4 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 6 -c 2 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"stage_kernel|march_kernel" -s 6 -c 2 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_full.log

@@ -2,6 +2,7 @@
 import collections
 import csv
 import io
+import re
 import subprocess
 import sys
 
@@ -69,7 +70,8 @@ for k, c in per.items():
     print("==", k[:50], f"warp-inst/cell {tot / cells:.2f}")
     print("  " + ", ".join(f"{o} {n / cells:.2f}" for o, n in c.most_common(22)))
     for name in summary["kernels"]:
-        if ("<0>" in name) == ("(bool)0" in k):
+        corr = lambda n: re.search(r"_kernel<(\(bool\))?(1|true)\b", n) is not None
+        if corr(name) == corr(k):
             summary["kernels"][name]["warp_inst_per_cell"] = tot / cells
             summary["kernels"][name]["opcode_mix_per_cell"] = {o: round(n / cells, 3) for o, n in c.most_common(30)}
 if json_out:
