@@ -276,22 +276,37 @@ int swof_workspace_size(const swof_params* p, size_t* bytes) {
 }
 
 // Picks the stage kernels for the context's physics and options and their launch shape: the marching
-// kernel (swof_march.cuh) by default; the tiled stage_kernel for the fused halo push and the dry-tile skip.
+// kernel (swof_march.cuh), or the tiled stage_kernel in SWOF_MARCH=0 builds.
 static int choose_kernels(swof_ctx* c) {
     const KParams& k = c->kp;
     const bool ff = c->kb.fric != nullptr;
     const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
     const bool push = c->kb.push_any != 0, dry = c->p.dry_skip != 0;
 #if SWOF_MARCH
-    if (!push && !dry) {
-        c->kpred = select_march<false>(k.fk, k.ga != 0, ff, generic);
-        c->kcorr = select_march<true>(k.fk, k.ga != 0, ff, generic);
-        // rows per warp: 64 (2 halo rows of slopes and faces per 64; a wave model chasing the tail of the
-        // last wave measured no better)
-        const char* fixed = getenv("SWOF_MARCH_H");
-        const int mh = fixed && atoi(fixed) > 0 ? atoi(fixed) : 64;
+    if (!(dry && getenv("SWOF_DRY_TILED"))) {               // (experiment: the tiled kernel's dry skip)
+        c->kpred = select_march<false>(k.fk, k.ga != 0, ff, generic, push, dry);
+        c->kcorr = select_march<true>(k.fk, k.ga != 0, ff, generic, push, dry);
+        // rows per warp segment, 8..64: minimise (waves of segments over the resident warp slots) x (rows +
+        // ~3 rows of halo work per segment) -- small grids get short segments to fill the 148 SMs
+        int occ_p = 0, occ_c = 0, dev = 0, nsm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, c->kpred, M_NW * 32, 0);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, c->kcorr, M_NW * 32, 0);
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return cuda_fail(c, e, "march kernel occupancy");
+        const long long slots = (long long)(occ_p < occ_c ? occ_p : occ_c) * nsm * M_NW;
+        const long long nstrip = (k.nx + M_OWN - 1) / M_OWN;
+        int mh = 64;
+        double best = 1e300;
+        for (int h = 8; h <= 64; ++h) {
+            const long long items = nstrip * ((k.ny + h - 1) / h);
+            const double cost = (double)((items + slots - 1) / (slots > 0 ? slots : 1)) * (h + 3);
+            if (cost < best) { best = cost; mh = h; }
+        }
+        const char* fixed = getenv("SWOF_MARCH_H");       // experiments
+        if (fixed && atoi(fixed) > 0) mh = atoi(fixed);
         c->kp.march_h = mh;
-        const long long nwarps = (long long)((k.nx + M_OWN - 1) / M_OWN) * ((k.ny + mh - 1) / mh);
+        const long long nwarps = nstrip * ((k.ny + mh - 1) / mh);
         c->sgrid = dim3((unsigned)((nwarps + M_NW - 1) / M_NW));
         c->sblock = dim3(M_NW * 32);
         c->ssmem = 0;

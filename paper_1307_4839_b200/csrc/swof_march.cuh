@@ -4,7 +4,7 @@
 // through warp shuffles (neighbour primitives, the left cell's high face, the east face's flux), so there
 // is no shared-memory tile and no CTA barrier in the stencil.  Same arithmetic as stage_kernel (the
 // canonical sheet of DESIGN.md §3), hence the same bits.  The default stage kernel (SWOF_MARCH=1); the tiled
-// stage_kernel stays for the fused halo push and the dry-tile skip.
+// stage_kernel (SWOF_MARCH=0 builds) is the shared-memory alternative.
 #pragma once
 
 namespace swof {
@@ -22,9 +22,6 @@ constexpr int M_OWN = 28;              // own columns per warp
 #define M_SLOW(...) __any_sync(0xffffffffu, (__VA_ARGS__))
 #else
 #define M_SLOW(...) (__VA_ARGS__)
-#endif
-#ifndef SWOF_MARCH_UNCOND
-#define SWOF_MARCH_UNCOND 0
 #endif
 #ifndef SWOF_MARCH_SCV
 #define SWOF_MARCH_SCV 0
@@ -95,7 +92,11 @@ __device__ __forceinline__ void march_fetch(const KParams& P, const KBufs& B, co
     }
 }
 
-template <bool CORRECTOR, class PH>
+// PUSH: also store the boundary rows into the neighbour strips' ghost rows (push_halo);
+// DRY: skip a face flux when both cells of every face of the warp's row hold h = 0 exactly (opt-in
+// swof_params.dry_skip; a dry cell reconstructs to depth 0 whatever its neighbours, so the face's flux and
+// interface sources are zero and the update reads zeros -- value-identical)
+template <bool CORRECTOR, class PH, bool PUSH = false, bool DRY = false>
 __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const KParams P, const KBufs B, const int par) {
     __shared__ double s_sc[6];
     __shared__ Ghost s_g;
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         FaceIn plusA;
         double2 sfa = make_double2(0.0, 0.0), sfb = make_double2(0.0, 0.0), slA = make_double2(0.0, 0.0);
         plusA.h = plusA.e = plusA.z = plusA.n = plusA.t = 0.0;
+        bool dA = DRY && __all_sync(0xffffffffu, A.h == 0.0), dB = DRY && __all_sync(0xffffffffu, Bw.h == 0.0);
 _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
         for (int j = j0; j <= jend + 1; ++j) {
             prim(rh_, rhu, rhv, rz, C);
@@ -222,44 +224,50 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                 Ahv0 = B.Ahv[o];
                 if (ph_ga<PH>(P)) VA0 = B.VA[o];
             }
-            // y slopes and y reconstruction of row m = j-1 (normal v, transverse u)
-            const double2 saB = ord1 ? z2 : half_slopes(A.h, Bw.h, C.h, A.e, Bw.e, C.e);
-            const double2 sbB = ord1 ? z2 : half_slopes(A.v, Bw.v, C.v, A.u, Bw.u, C.u);
-            const FaceIn minusB = recon_minus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
-            const FaceIn plusB = recon_plus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
-#if SWOF_MARCH_UNCOND
-            {   // computed from j0 on (the first two rows' results are discarded): one straight loop body
-#else
+            // DRY: warp rows whose 32 cells all hold h = 0 (carried: dA, dB of rows j-2, j-1; dC of row j)
+            const bool dC = DRY && __all_sync(0xffffffffu, C.h == 0.0);
+            // y slopes and y reconstruction of row m = j-1 (normal v, transverse u); not needed when rows
+            // j-2..j are dry (both of row j-1's faces are dry-dry, its Fc_y multiplies a zero depth)
+            double2 saB = z2, sbB = z2;
+            FaceIn minusB = {0.0, 0.0, 0.0, 0.0, 0.0}, plusB = {0.0, 0.0, 0.0, 0.0, 0.0};
+            if (!(DRY && dA && dB && dC)) {
+                saB = ord1 ? z2 : half_slopes(A.h, Bw.h, C.h, A.e, Bw.e, C.e);
+                sbB = ord1 ? z2 : half_slopes(A.v, Bw.v, C.v, A.u, Bw.u, C.u);
+                minusB = recon_minus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
+                plusB = recon_plus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
+            }
             if (j - 1 >= j0) {
-#endif
                 // y face between rows j-2 and j-1: the north face of row j-2, the south face of row j-1
-                double2 nfa, nfb;
-                if (M_SLOW(face_flux<false>(P.g, h_eps, plusA, minusB, nfa, nfb, rus)))
-                    face_flux<true>(P.g, h_eps, plusA, minusB, nfa, nfb, rus);
-#if SWOF_MARCH_UNCOND
-                {
-#else
+                double2 nfa = z2, nfb = z2;
+                if (!(DRY && dA && dB)) {
+                    if (M_SLOW(face_flux<false>(P.g, h_eps, plusA, minusB, nfa, nfb, rus)))
+                        face_flux<true>(P.g, h_eps, plusA, minusB, nfa, nfb, rus);
+                }
                 if (j - 2 >= j0) {
-#endif
                     // ---- finalise row f = j-2 (window A): x direction by shuffles, update, sources ----
-                    const double2 heA = make_double2(A.h, A.e);
-                    const double2 cL = shup2(heA), cR = shdn2(heA);
-                    const double2 uvA = make_double2(A.u, A.v);
-                    const double2 uL = shup2(uvA), uR = shdn2(uvA);
-                    const double2 sa = ord1 ? z2 : half_slopes(cL.x, A.h, cR.x, cL.y, A.e, cR.y);
-                    const double2 sb = ord1 ? z2 : half_slopes(uL.x, A.u, uR.x, uL.y, A.v, uR.y);
-                    const FaceIn pl = recon_plus(heA, A.u, A.v, A.rh, sa, sb);
-                    const FaceIn mi = recon_minus(heA, A.u, A.v, A.rh, sa, sb);
-                    FaceIn lp;                                // the west neighbour's high face
-                    lp.h = shup(pl.h);
-                    lp.e = shup(pl.e);
-                    lp.z = shup(pl.z);
-                    lp.n = shup(pl.n);
-                    lp.t = shup(pl.t);
-                    double2 wa, wb;                           // west face of this lane's cell
-                    if (M_SLOW(face_flux<false>(P.g, h_eps, lp, mi, wa, wb, rus))) face_flux<true>(P.g, h_eps, lp, mi, wa, wb, rus);
-                    const double2 ea = shdn2(wa), eb = shdn2(wb);
-                    const double Fcx = centred_source(g2, A.h, A.e, sa.x, sa.y);
+                    double2 wa = z2, wb = z2, ea = z2, eb = z2;   // west / east face of this lane's cell
+                    double Fcx = 0.0;
+                    if (!(DRY && dA)) {                       // a dry row: every x face is dry-dry
+                        const double2 heA = make_double2(A.h, A.e);
+                        const double2 cL = shup2(heA), cR = shdn2(heA);
+                        const double2 uvA = make_double2(A.u, A.v);
+                        const double2 uL = shup2(uvA), uR = shdn2(uvA);
+                        const double2 sa = ord1 ? z2 : half_slopes(cL.x, A.h, cR.x, cL.y, A.e, cR.y);
+                        const double2 sb = ord1 ? z2 : half_slopes(uL.x, A.u, uR.x, uL.y, A.v, uR.y);
+                        const FaceIn pl = recon_plus(heA, A.u, A.v, A.rh, sa, sb);
+                        const FaceIn mi = recon_minus(heA, A.u, A.v, A.rh, sa, sb);
+                        FaceIn lp;                            // the west neighbour's high face
+                        lp.h = shup(pl.h);
+                        lp.e = shup(pl.e);
+                        lp.z = shup(pl.z);
+                        lp.n = shup(pl.n);
+                        lp.t = shup(pl.t);
+                        if (M_SLOW(face_flux<false>(P.g, h_eps, lp, mi, wa, wb, rus)))
+                            face_flux<true>(P.g, h_eps, lp, mi, wa, wb, rus);
+                        ea = shdn2(wa);
+                        eb = shdn2(wb);
+                        Fcx = centred_source(g2, A.h, A.e, sa.x, sa.y);
+                    }
                     const double pxm = lx * (ea.x - wa.x);
                     const double qx = lx * ((ea.y - wb.x) - Fcx), qy = lx * (eb.y - wb.y);
                     // y half with the south (carried) and north (just computed) faces
@@ -290,6 +298,7 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                             B.Bhu[o] = hu2;
                             B.Bhv[o] = hv2;
                             if (ph_ga<PH>(P)) B.VB[o] = Vn;
+                            if (PUSH && (f < GHOST_ROWS || f >= ny - GHOST_ROWS)) push_halo(B, 1, ny, pitch, f, gi, hst, hu2, hv2);
                         } else {
                             const double hN = 0.5 * (Ah0 + hst);
                             const double huN = 0.5 * (Ahu0 + hu2);
@@ -298,6 +307,7 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                             B.Ahu[o] = huN;
                             B.Ahv[o] = hvN;
                             if (ph_ga<PH>(P)) B.VA[o] = 0.5 * (VA0 + Vn);
+                            if (PUSH && (f < GHOST_ROWS || f >= ny - GHOST_ROWS)) push_halo(B, 0, ny, pitch, f, gi, hN, huN, hvN);
                             if (P.cfl_mode == 0) {   // own lanes only (divergent: no warp vote here)
                                 double su, sv;
                                 if (cfl_speeds<false>(P, hN, huN, hvN, su, sv)) cfl_speeds<true>(P, hN, huN, hvN, su, sv);
@@ -311,6 +321,8 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                 sfb = nfb;
             }
             // slide the window
+            dA = dB;
+            dB = dC;
             plusA = plusB;
             slA = saB;
             A = Bw;
@@ -348,17 +360,27 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
     }
 }
 
-template <bool C, int FK, bool GA, bool FF>
-constexpr StageFn march_fn() { return march_kernel<C, Phys<FK, GA, FF>>; }
-template <bool C>
-__host__ inline StageFn select_march(int fk, bool ga, bool ff, bool generic) {
-    if (generic) return march_kernel<C, PhysRT>;
+template <bool C, int FK, bool GA, bool FF, bool DRY>
+constexpr StageFn march_fn() { return march_kernel<C, Phys<FK, GA, FF>, false, DRY>; }
+template <bool C, bool D>
+__host__ inline StageFn march_spec(int fk, bool ga, bool ff) {
     static const StageFn tab[3][2][2] = {
-        {{march_fn<C, 0, false, false>(), march_fn<C, 0, false, true>()}, {march_fn<C, 0, true, false>(), march_fn<C, 0, true, true>()}},
-        {{march_fn<C, 1, false, false>(), march_fn<C, 1, false, true>()}, {march_fn<C, 1, true, false>(), march_fn<C, 1, true, true>()}},
-        {{march_fn<C, 2, false, false>(), march_fn<C, 2, false, true>()}, {march_fn<C, 2, true, false>(), march_fn<C, 2, true, true>()}},
+        {{march_fn<C, 0, false, false, D>(), march_fn<C, 0, false, true, D>()},
+         {march_fn<C, 0, true, false, D>(), march_fn<C, 0, true, true, D>()}},
+        {{march_fn<C, 1, false, false, D>(), march_fn<C, 1, false, true, D>()},
+         {march_fn<C, 1, true, false, D>(), march_fn<C, 1, true, true, D>()}},
+        {{march_fn<C, 2, false, false, D>(), march_fn<C, 2, false, true, D>()},
+         {march_fn<C, 2, true, false, D>(), march_fn<C, 2, true, true, D>()}},
     };
     return tab[fk][ga][ff];
+}
+// the default scheme runs physics-specialised instances (with or without the dry skip); the generic
+// PhysRT instance serves the scheme variants and the fused halo push
+template <bool C>
+__host__ inline StageFn select_march(int fk, bool ga, bool ff, bool generic, bool push = false, bool dry = false) {
+    if (push) return dry ? march_kernel<C, PhysRT, true, true> : march_kernel<C, PhysRT, true>;
+    if (generic) return dry ? march_kernel<C, PhysRT, false, true> : march_kernel<C, PhysRT>;
+    return dry ? march_spec<C, true>(fk, ga, ff) : march_spec<C, false>(fk, ga, ff);
 }
 
 }  // namespace swof
