@@ -14,7 +14,7 @@ from workloads import make  # noqa: E402
 torch.cuda.set_device(0)
 CASES = [("cfg4", {"flux": "rusanov", "cfl": 0.25}, 50), ("cfg4", {"order": 1, "cfl": 1.0}, 50),
          ("cfg4", {"cfl_mode": "face"}, 50), ("cfg4", {"ga_form": "darcy"}, 50)] if "--variants" in sys.argv else [
-         ("cfg0", {}, 200), ("cfg1", {}, 200), ("cfg2", {}, 100), ("cfg3", {}, 100), ("cfg3", {"dry_skip": 1}, 100), ("cfg3", {"dry_skip": 1, "_env": "SWOF_DRY_TILED"}, 100),
+         ("cfg0", {}, 200), ("cfg1", {}, 200), ("cfg2", {}, 100), ("cfg3", {}, 100), ("cfg3", {"dry_skip": 1}, 100),
          ("cfg4", {}, 50), ("cfg4", {"dry_skip": 1}, 50),
          ("cfg4", {"flux": "rusanov", "cfl": 0.25}, 50), ("cfg4", {"order": 1, "cfl": 1.0}, 50),
          ("cfg4", {"cfl_mode": "face"}, 50), ("cfg4", {"ga_form": "darcy"}, 50)]
