@@ -286,7 +286,7 @@ static int choose_kernels(swof_ctx* c) {
     if (!dry) {                                          // the dry skip runs the tiled kernel (§5)
         c->kpred = select_march<false>(k.fk, k.ga != 0, ff, generic, push);
         c->kcorr = select_march<true>(k.fk, k.ga != 0, ff, generic, push);
-        // rows per warp segment, 8..64: minimise (waves of segments over the resident warp slots) x (rows +
+        // rows per warp segment, 1..64: minimise (waves of segments over the resident warp slots) x (rows +
         // ~3 rows of halo work per segment) -- small grids get short segments to fill the 148 SMs
         int occ_p = 0, occ_c = 0, dev = 0, nsm = 0;
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, c->kpred, M_NW * 32, 0);
@@ -298,7 +298,7 @@ static int choose_kernels(swof_ctx* c) {
         const long long nstrip = (k.nx + M_OWN - 1) / M_OWN;
         int mh = 64;
         double best = 1e300;
-        for (int h = 8; h <= 64; ++h) {
+        for (int h = 1; h <= 64; ++h) {
             const long long items = nstrip * ((k.ny + h - 1) / h);
             const double cost = (double)((items + slots - 1) / (slots > 0 ? slots : 1)) * (h + 3);
             if (cost < best) { best = cost; mh = h; }
