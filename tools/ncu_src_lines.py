@@ -1,7 +1,7 @@
 """Per-source-line ncu attribution of a kernel's SASS: instructions executed and stall samples by the
 outermost line of the kernel body (the call site in KFILE) and by the innermost line (the helper).
 
-    python tools/ncu_src_lines.py REPORT.ncu-rep LIB.so KFILE MANGLED_SUBSTR [NCU_KERNEL_REGEX]
+    python tools/ncu_src_lines.py REPORT.ncu-rep LIB.so KFILE MANGLED_SUBSTR [NCU_KERNEL_REGEX [OPCODE_PREFIX]]
 
 e.g. tools/ncu_src_lines.py gpurun_out/prof.ncu-rep paper_1307_4839_b200/libswof.so swof_march.cuh \
          march_kernelILb0ENS_4PhysILi1ELb1ELb0E 'march_kernel<\\(bool\\)0'
@@ -18,6 +18,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 rep, lib, kfile, mangled = sys.argv[1:5]
 kregex = sys.argv[5] if len(sys.argv) > 5 else None
+opfilter = sys.argv[6] if len(sys.argv) > 6 else None      # count only SASS opcodes starting with this
 srcs = {}
 
 
@@ -75,12 +76,15 @@ for r in csv.reader(io.StringIO(sass)):
         o, i = info.get(a - base, (None, None))
         smp = int(r[h.index("Warp Stall Sampling (All Samples)")] or 0)
         ins = int(r[h.index("Instructions Executed")] or 0)
+        if opfilter:
+            op = r[h.index("Source")].strip()
+            op = op.split(None, 1)[1] if op.startswith("@") else op
+            if not op.startswith(opfilter):
+                continue
         per_outer[o][0] += smp
         per_outer[o][1] += ins
         per_inner[i][0] += smp
         per_inner[i][1] += ins
-    if take and kern and len(r) > 5 and kregex is None:
-        pass
 for title, d in (("call site (" + kfile + ")", per_outer), ("innermost line", per_inner)):
     ts = sum(v[0] for v in d.values()) or 1
     ti = sum(v[1] for v in d.values()) or 1
