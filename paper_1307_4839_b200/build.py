@@ -15,7 +15,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libswof.so"
 SOURCES = [CSRC / "swof.cu"]
-DEPS = SOURCES + [CSRC / "swof_kernels.cuh", CSRC / "swof_d8.cuh", CSRC / "swof_march.cuh", CSRC / "swof_pair.cuh", ROOT / "include" / "swof.h"]
+DEPS = SOURCES + [CSRC / "swof_kernels.cuh", CSRC / "swof_d8.cuh", CSRC / "swof_march.cuh", ROOT / "include" / "swof.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [

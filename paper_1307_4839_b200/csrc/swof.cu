@@ -22,12 +22,6 @@
 #if SWOF_MARCH
 #include "swof_march.cuh"
 #endif
-#ifndef SWOF_PAIR
-#define SWOF_PAIR 0                    // 1: the warp-pair split of the marching kernel (swof_pair.cuh, experiment)
-#endif
-#if SWOF_PAIR
-#include "swof_pair.cuh"
-#endif
 
 using namespace swof;
 
@@ -316,14 +310,6 @@ static int choose_kernels(swof_ctx* c) {
         c->sgrid = dim3((unsigned)((nwarps + M_NW - 1) / M_NW));
         c->sblock = dim3(M_NW * 32);
         c->ssmem = 0;
-#if SWOF_PAIR
-        if (!push) {
-            c->kpred = select_pair<false>(k.fk, k.ga != 0, ff, generic);
-            c->kcorr = select_pair<true>(k.fk, k.ga != 0, ff, generic);
-            c->sgrid = dim3((unsigned)((nwarps + PR_NP - 1) / PR_NP));
-            c->sblock = dim3(PR_NW * 32);
-        }
-#endif
         return SWOF_OK;
     }
 #endif
