@@ -61,10 +61,13 @@ sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-s
 per_outer = collections.defaultdict(lambda: [0, 0])
 per_inner = collections.defaultdict(lambda: [0, 0])
 kern, take, base = None, False, None
+seen = set()
 for r in csv.reader(io.StringIO(sass)):
     if r and r[0] == "Kernel Name":
         kern = r[1]
-        take = kregex is None or re.search(kregex, kern) is not None
+        # the page lists each kernel twice; count the first listing only
+        take = (kregex is None or re.search(kregex, kern) is not None) and kern not in seen
+        seen.add(kern)
         base = None
         continue
     if r and r[0] == "Address":
