@@ -276,16 +276,16 @@ int swof_workspace_size(const swof_params* p, size_t* bytes) {
 }
 
 // Picks the stage kernels for the context's physics and options and their launch shape: the marching
-// kernel (swof_march.cuh); the tiled stage_kernel for the opt-in dry skip and in SWOF_MARCH=0 builds.
+// kernel (swof_march.cuh); the tiled stage_kernel in SWOF_MARCH=0 builds.
 static int choose_kernels(swof_ctx* c) {
     const KParams& k = c->kp;
     const bool ff = c->kb.fric != nullptr;
     const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
     const bool push = c->kb.push_any != 0, dry = c->p.dry_skip != 0;
 #if SWOF_MARCH
-    if (!dry) {                                          // the dry skip runs the tiled kernel (§5)
-        c->kpred = select_march<false>(k.fk, k.ga != 0, ff, generic, push);
-        c->kcorr = select_march<true>(k.fk, k.ga != 0, ff, generic, push);
+    {
+        c->kpred = select_march<false>(k.fk, k.ga != 0, ff, generic, push, dry);
+        c->kcorr = select_march<true>(k.fk, k.ga != 0, ff, generic, push, dry);
         // rows per warp segment, 1..64: minimise (waves of segments over the resident warp slots) x (rows +
         // ~3 rows of halo work per segment) -- small grids get short segments to fill the 148 SMs
         int occ_p = 0, occ_c = 0, dev = 0, nsm = 0;

@@ -92,10 +92,13 @@ __device__ __forceinline__ void march_fetch(const KParams& P, const KBufs& B, co
     }
 }
 
-// PUSH: also store the boundary rows into the neighbour strips' ghost rows (push_halo).
-// (The opt-in dry skip runs the tiled stage_kernel: a dry-row skip here, by warp votes, measured 12.8 G
-// cell-updates/s on cfg3 against the tiled kernel's 14.1 G.)
-template <bool CORRECTOR, class PH, bool PUSH = false>
+// PUSH: also store the boundary rows into the neighbour strips' ghost rows (push_halo);
+// DRY (opt-in swof_params.dry_skip): warp votes on rows whose 32 cells hold h = 0 exactly skip the faces of
+// a dry row pair, the y stencil of three dry rows and the x stencil of a dry row.  A dry cell reconstructs
+// to depth 0 whatever its neighbours (minmod of (-h_m, h_p) is 0), so those fluxes and sources are zero and
+// the update reads zeros -- value-identical.  Measured: cfg3 12.0 -> 13.7 G cell-updates/s, and on the wet
+// cfg4 it costs 6-10 % (the tiled kernel's tile skip: 14.1 G and 26 %).
+template <bool CORRECTOR, class PH, bool PUSH = false, bool DRY = false>
 __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const KParams P, const KBufs B, const int par) {
     __shared__ double s_sc[6];
     __shared__ Ghost s_g;
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         // recomputing them)
         long long onx = (long long)(j0 + 1) * pitch + gi;
         long long ofn = (long long)(j0 - 2) * pitch + gi;
+        bool dA = DRY && __all_sync(0xffffffffu, A.h == 0.0), dB = DRY && __all_sync(0xffffffffu, Bw.h == 0.0);
 _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
         for (int j = j0; j <= jend + 1; ++j) {
             prim(rh_, rhu, rhv, rz, C);
@@ -228,21 +232,30 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                 Ahv0 = B.Ahv[o];
                 if (ph_ga<PH>(P)) VA0 = B.VA[o];
             }
-            // y slopes and y reconstruction of row m = j-1 (normal v, transverse u)
-            const double2 saB = ord1 ? z2 : half_slopes(A.h, Bw.h, C.h, A.e, Bw.e, C.e);
-            const double2 sbB = ord1 ? z2 : half_slopes(A.v, Bw.v, C.v, A.u, Bw.u, C.u);
-            const FaceIn minusB = recon_minus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
-            const FaceIn plusB = recon_plus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
+            // DRY: warp rows whose 32 cells all hold h = 0 (carried: dA, dB of rows j-2, j-1; dC of row j)
+            const bool dC = DRY && __all_sync(0xffffffffu, C.h == 0.0);
+            // y slopes and y reconstruction of row m = j-1 (normal v, transverse u); not needed when rows
+            // j-2..j are dry (both of row j-1's faces are dry-dry, its Fc_y multiplies a zero depth)
+            double2 saB = z2, sbB = z2;
+            FaceIn minusB = {0.0, 0.0, 0.0, 0.0, 0.0}, plusB = {0.0, 0.0, 0.0, 0.0, 0.0};
+            if (!(DRY && dA && dB && dC)) {
+                saB = ord1 ? z2 : half_slopes(A.h, Bw.h, C.h, A.e, Bw.e, C.e);
+                sbB = ord1 ? z2 : half_slopes(A.v, Bw.v, C.v, A.u, Bw.u, C.u);
+                minusB = recon_minus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
+                plusB = recon_plus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
+            }
             if (j - 1 >= j0) {
                 // y face between rows j-2 and j-1: the north face of row j-2, the south face of row j-1
-                double2 nfa, nfb;
-                if (M_SLOW(face_flux<false>(P.g, h_eps, plusA, minusB, nfa, nfb, rus)))
-                    face_flux<true>(P.g, h_eps, plusA, minusB, nfa, nfb, rus);
+                double2 nfa = z2, nfb = z2;
+                if (!(DRY && dA && dB)) {
+                    if (M_SLOW(face_flux<false>(P.g, h_eps, plusA, minusB, nfa, nfb, rus)))
+                        face_flux<true>(P.g, h_eps, plusA, minusB, nfa, nfb, rus);
+                }
                 if (j - 2 >= j0) {
                     // ---- finalise row f = j-2 (window A): x direction by shuffles, update, sources ----
-                    double2 wa, wb, ea, eb;                   // west / east face of this lane's cell
-                    double Fcx;
-                    {
+                    double2 wa = z2, wb = z2, ea = z2, eb = z2;   // west / east face of this lane's cell
+                    double Fcx = 0.0;
+                    if (!(DRY && dA)) {                       // a dry row: every x face is dry-dry
                         const double2 heA = make_double2(A.h, A.e);
                         const double2 cL = shup2(heA), cR = shdn2(heA);
                         const double2 uvA = make_double2(A.u, A.v);
@@ -316,6 +329,8 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                 sfb = nfb;
             }
             // slide the window
+            dA = dB;
+            dB = dC;
             plusA = plusB;
             slA = saB;
             A = Bw;
@@ -353,20 +368,27 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
     }
 }
 
-template <bool C, int FK, bool GA, bool FF>
-constexpr StageFn march_fn() { return march_kernel<C, Phys<FK, GA, FF>>; }
-// the default scheme runs physics-specialised instances; the generic PhysRT instance serves the scheme
-// variants and the fused halo push
-template <bool C>
-__host__ inline StageFn select_march(int fk, bool ga, bool ff, bool generic, bool push = false) {
-    if (push) return march_kernel<C, PhysRT, true>;
-    if (generic) return march_kernel<C, PhysRT>;
+template <bool C, int FK, bool GA, bool FF, bool DRY>
+constexpr StageFn march_fn() { return march_kernel<C, Phys<FK, GA, FF>, false, DRY>; }
+template <bool C, bool D>
+__host__ inline StageFn march_spec(int fk, bool ga, bool ff) {
     static const StageFn tab[3][2][2] = {
-        {{march_fn<C, 0, false, false>(), march_fn<C, 0, false, true>()}, {march_fn<C, 0, true, false>(), march_fn<C, 0, true, true>()}},
-        {{march_fn<C, 1, false, false>(), march_fn<C, 1, false, true>()}, {march_fn<C, 1, true, false>(), march_fn<C, 1, true, true>()}},
-        {{march_fn<C, 2, false, false>(), march_fn<C, 2, false, true>()}, {march_fn<C, 2, true, false>(), march_fn<C, 2, true, true>()}},
+        {{march_fn<C, 0, false, false, D>(), march_fn<C, 0, false, true, D>()},
+         {march_fn<C, 0, true, false, D>(), march_fn<C, 0, true, true, D>()}},
+        {{march_fn<C, 1, false, false, D>(), march_fn<C, 1, false, true, D>()},
+         {march_fn<C, 1, true, false, D>(), march_fn<C, 1, true, true, D>()}},
+        {{march_fn<C, 2, false, false, D>(), march_fn<C, 2, false, true, D>()},
+         {march_fn<C, 2, true, false, D>(), march_fn<C, 2, true, true, D>()}},
     };
     return tab[fk][ga][ff];
+}
+// the default scheme runs physics-specialised instances (with or without the dry skip); the generic
+// PhysRT instance serves the scheme variants and the fused halo push
+template <bool C>
+__host__ inline StageFn select_march(int fk, bool ga, bool ff, bool generic, bool push = false, bool dry = false) {
+    if (push) return dry ? march_kernel<C, PhysRT, true, true> : march_kernel<C, PhysRT, true>;
+    if (generic) return dry ? march_kernel<C, PhysRT, false, true> : march_kernel<C, PhysRT>;
+    return dry ? march_spec<C, true>(fk, ga, ff) : march_spec<C, false>(fk, ga, ff);
 }
 
 }  // namespace swof

@@ -1,5 +1,5 @@
 """The tiled stage kernel (csrc/swof_kernels.cuh: shared-memory tile) is the library's kernel in
-SWOF_MARCH=0 builds and serves the opt-in dry skip in the default one.  This rebuilds the library with
+SWOF_MARCH=0 builds.  This rebuilds the library with
 SWOF_MARCH=0 and runs the one-step and predictor-stage parity tests of test_gpu_parity.py through it, in a
 subprocess pointed at that build (SWOF_LIB)."""
 import os

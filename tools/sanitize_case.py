@@ -1,6 +1,6 @@
 """Small end-to-end run of every kernel for compute-sanitizer: cfg0 (walls) and a 256^2
-cfg4 case through the graph path, a variant case (generic instance, order-1 commit, face CFL), the tiled
-kernel (dry skip), 2 row strips
+cfg4 case through the graph path, a variant case (generic instance, order-1 commit, face CFL), the dry-row
+skip, 2 row strips
 (fused push), the D8 kernel (fp32 and fp64) and the math self-test."""
 import sys
 
@@ -18,7 +18,7 @@ torch.cuda.set_device(0)
 for name, nx, ny, steps, kw in (("cfg0", None, None, 20, {}), ("cfg4", 256, 256, 20, {}),
                                 ("cfg3", 130, 90, 10, {"flux": "rusanov", "order": 1, "cfl": 1.0, "cfl_mode": "face",
                                                        "ga_form": "darcy"}),
-                                ("cfg3", 130, 90, 10, {"dry_skip": 1})):    # the tiled kernel (dry skip)
+                                ("cfg3", 130, 90, 10, {"dry_skip": 1})):    # the dry-row skip instances
     cfg = make(name, nx=nx, ny=ny)
     for k, v in kw.items():
         setattr(cfg, k, v)
