@@ -111,9 +111,9 @@ typedef struct swof_params {
     double inflow_width[4];  /* width W [m] that Q(t) is spread over per side (0: the segment's own
                                 (k1 - k0) * dy or dx); a strip of a decomposed grid passes the global
                                 segment's width and its share of Q so that q = Q/W is unchanged   */
-    int32_t dry_skip;        /* 1: tiles whose cells and halo all hold h = 0 exactly skip the stencil
-                                work (results unchanged); pays on mostly dry domains (cfg3: +56 %),
-                                costs ~3 % on wet ones, so off by default                          */
+    int32_t dry_skip;        /* 1: rows of a warp's strip whose cells all hold h = 0 exactly skip the
+                                face and slope work (results unchanged); pays on mostly dry domains
+                                (cfg3: +14 %), costs 6-10 % on wet ones, so off by default        */
 } swof_params;
 
 typedef struct swof_diag {
