@@ -1,10 +1,12 @@
-// swof_march.cuh -- an alternative stage kernel that keeps the stencil in registers: each warp owns a
-// strip of 28 columns (lanes 2..29 of the 32 columns i0-2 .. i0+29) and marches down MH rows.  The
-// y-direction (slopes, reconstruction, faces) lives in a 3-row register window, the x-direction goes
+// swof_march.cuh -- the stage kernel (predictor and corrector of Algorithm 1's Heun step) with
+// the stencil in registers: each warp (one per CTA) owns a strip of 28 columns (lanes 2..29 of the 32
+// columns i0-2 .. i0+29) and marches down a segment of rows (KParams::march_h, chosen at create time).  The
+// y direction (slopes, reconstruction, faces) lives in a 3-row register window, the x direction goes
 // through warp shuffles (neighbour primitives, the left cell's high face, the east face's flux), so there
-// is no shared-memory tile and no CTA barrier in the stencil.  Same arithmetic as stage_kernel (the
-// canonical sheet of DESIGN.md §3), hence the same bits.  The default stage kernel (SWOF_MARCH=1); the tiled
-// stage_kernel (SWOF_MARCH=0 builds) is the shared-memory alternative.
+// is no shared-memory tile and no barrier in the stencil.  Same arithmetic as the oracle and as the tiled
+// stage_kernel (the canonical sheet of DESIGN.md §3), hence the same bits.  Default (SWOF_MARCH=1); the
+// tiled stage_kernel of swof_kernels.cuh runs in SWOF_MARCH=0 builds.  DESIGN.md §5 has the design and
+// its measurements, §8 the rejected variants (their switches below stay off).
 #pragma once
 
 namespace swof {
