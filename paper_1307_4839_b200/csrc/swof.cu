@@ -306,7 +306,20 @@ static int choose_kernels(swof_ctx* c) {
         const char* fixed = getenv("SWOF_MARCH_H");       // experiments
         if (fixed && atoi(fixed) > 0) mh = atoi(fixed);
         c->kp.march_h = mh;
-        const long long nwarps = nstrip * ((k.ny + mh - 1) / mh);
+        // the last wave of segments is cut shorter (mh/4 rows) so that the SMs run dry together
+        int g1 = (k.ny + mh - 1) / mh, h2 = mh;
+        const char* tail = getenv("SWOF_MARCH_TAIL");
+        if (!(tail && atoi(tail) == 0) && mh >= 8) {
+            h2 = mh / 4;
+            const long long g2 = (slots + nstrip - 1) / nstrip;            // one wave of short segments
+            const long long rows_tail = g2 * h2;
+            const long long g1m = (k.ny - rows_tail) / mh;
+            if (g1m >= 1) g1 = (int)g1m; else h2 = mh;
+        }
+        c->kp.march_g1 = g1;
+        c->kp.march_h2 = h2;
+        const long long nseg = g1 + (k.ny - (long long)g1 * mh + h2 - 1) / h2;
+        const long long nwarps = nstrip * (k.ny > (long long)g1 * mh ? nseg : g1);
         c->sgrid = dim3((unsigned)((nwarps + M_NW - 1) / M_NW));
         c->sblock = dim3(M_NW * 32);
         c->ssmem = 0;

@@ -41,6 +41,18 @@ constexpr int M_NW = SWOF_MARCH_NW;    // warps per CTA (independent); rows per 
 
 struct MPrim { double h, e, u, v, rh; };
 
+// rows [j0, jend) of segment row g: march_h rows high, the last wave's segments march_h2 rows high
+__device__ __forceinline__ void march_seg(const KParams& P, int g, int& j0, int& jend) {
+    if (g < P.march_g1) {
+        j0 = g * P.march_h;
+        jend = j0 + P.march_h;
+    } else {
+        j0 = P.march_g1 * P.march_h + (g - P.march_g1) * P.march_h2;
+        jend = j0 + P.march_h2;
+    }
+    jend = jend < P.ny ? jend : P.ny;
+}
+
 __device__ __forceinline__ double2 shup2(double2 v) {
     return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
@@ -121,7 +133,9 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
     {
         const int nstrip0 = (P.nx + M_OWN - 1) / M_OWN;
         const int wid0 = blockIdx.x * M_NW + warp;
-        const int i00 = (wid0 % nstrip0) * M_OWN, j00 = (wid0 / nstrip0) * P.march_h;
+        int j00, jend0;
+        march_seg(P, wid0 / nstrip0, j00, jend0);
+        const int i00 = (wid0 % nstrip0) * M_OWN;
         early = i00 - HALO >= 0 && i00 - HALO + 32 <= P.nx && j00 >= 2 && j00 < P.ny;
         if (early) {
             size_t o = (size_t)(j00 - 2) * P.pitch + (i00 - HALO + lane);
@@ -186,7 +200,9 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
     const int nstrip = (nx + M_OWN - 1) / M_OWN;
     const int wid = blockIdx.x * M_NW + warp;
     const int s = wid % nstrip, g = wid / nstrip;
-    const int i0 = s * M_OWN, j0 = g * P.march_h;
+    const int i0 = s * M_OWN;
+    int j0, jend;
+    march_seg(P, g, j0, jend);
     double amx = 0.0, amy = 0.0;
     if (j0 < ny) {
         const double* __restrict__ in_h = CORRECTOR ? B.Bh : B.Ah;
@@ -198,7 +214,6 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         const double2 z2 = make_double2(0.0, 0.0);
         const int gi = i0 - HALO + lane;
         const bool own_col = lane >= HALO && lane < HALO + M_OWN && gi < nx;
-        const int jend = j0 + P.march_h < ny ? j0 + P.march_h : ny;
         const bool fastx = i0 - HALO >= 0 && i0 - HALO + 32 <= nx;   // all 32 columns inside (warp-uniform)
         auto prim = [&](double h, double hu, double hv, double z, MPrim& m) {
             const double rh = (h > h_eps) ? drcp(h) : 0.0;
