@@ -311,9 +311,11 @@ static int choose_kernels(swof_ctx* c) {
         int g1 = (k.ny + mh - 1) / mh, h2 = mh;
         const char* tail = getenv("SWOF_MARCH_TAIL");
         const long long waves = nstrip * (long long)g1 / (slots > 0 ? slots : 1);
-        if (!(tail && atoi(tail) == 0) && mh >= 8 && waves >= 4) {
+        const int tail_mode = tail ? atoi(tail) : 1;         // 0 off, 1 auto, 2 always (tests)
+        if (tail_mode != 0 && mh >= 8 && (waves >= 4 || tail_mode == 2)) {
             h2 = mh / 4;
-            const long long g2 = (slots + nstrip - 1) / nstrip;            // one wave of short segments
+            long long g2 = (slots + nstrip - 1) / nstrip;                  // one wave of short segments
+            if (tail_mode == 2) g2 = (k.ny / 2) / h2 > 0 ? (k.ny / 2) / h2 : 1;   // tests: half the rows
             const long long rows_tail = g2 * h2;
             const long long g1m = (k.ny - rows_tail) / mh;
             if (g1m >= 1) g1 = (int)g1m; else h2 = mh;

@@ -62,3 +62,16 @@ def test_march_inflow_on_segment_ends(gpu, monkeypatch, mh):
     r = oracle.run(cfg, nsteps=6)
     res = compare(g, r, 1e-11)
     assert res["bitwise"], res
+
+
+@pytest.mark.parametrize("mh", [8, 16])
+@pytest.mark.parametrize("name,nx,ny,bc", [("cfg4", 57, 130, None), ("cfg3", 84, 70, None), ("cfg4", 29, 40, "periodic_y")])
+def test_march_short_tail_segments(gpu, monkeypatch, mh, name, nx, ny, bc):
+    """The last wave's shorter segments (SWOF_MARCH_TAIL=2 forces them on grids this small)."""
+    monkeypatch.setenv("SWOF_MARCH_H", str(mh))
+    monkeypatch.setenv("SWOF_MARCH_TAIL", "2")
+    cfg = _case(name, nx, ny, bc)
+    g = gpu_run(cfg, nsteps=4)
+    r = oracle.run(cfg, nsteps=4)
+    res = compare(g, r, 1e-11)
+    assert res["bitwise"], res
