@@ -15,6 +15,8 @@ import json
 import math
 import os
 
+from decimal import Decimal, getcontext
+
 import numpy as np
 import pytest
 
@@ -180,6 +182,16 @@ def test_uniform_friction_recurrence():
         assert abs(r["hu"][0, 0] - 0.5 * (1.0 + q2)) <= 2e-16
         if "q_star" in ex:
             assert abs(q1 - ex["q_star"]) < 1e-10 and abs(q2 - ex["q_2star"]) < 1e-10
+        # the same closed form in 40-digit decimal arithmetic (h = 1, so h^(4/3) = 1 exactly): the oracle's
+        # fp64 result within 1e-14
+        getcontext().prec = 40
+        D = Decimal
+        dgcf = D(repr(G)) * D(repr(ex[coef])) ** 2 if law == "manning" else D(repr(ex[coef])) / 8
+        ddt = D(repr(ex["dt"]))
+        d1 = D(1) / (D(1) + ddt * dgcf * D(1))
+        d2 = d1 / (D(1) + ddt * dgcf * d1)
+        want = (D(1) + d2) / 2
+        assert abs(D(r["hu"][0, 0]) - want) <= D("1e-14"), (law, r["hu"][0, 0], want)
 
 
 def test_uniform_rain_green_ampt_recurrence():

@@ -244,6 +244,36 @@ def test_friction_manning_power():
         assert abs(a - want) <= 1e-14 * abs(want) + 1e-300
 
 
+def test_friction_sheet_vs_printed_division():
+    """DESIGN.md §3 Q11/Q20: the sheet evaluates the printed q* / (1 + w) as q* (1 / (1 + w)) -- one
+    reciprocal for the two discharge components of a 2D cell.  Equal in exact arithmetic; in fp64 the two
+    differ by at most 2 ulp (RN(1/d) then RN(q RN(1/d)) against the single RN(q/d)).  Pinned here against the
+    printed division evaluated independently in numpy with the same w (Darcy/Chezy: w = k/h*; Manning/
+    Strickler: w = k s^4 with s = icbrt(h*), icbrt itself pinned to libm cbrt in test_icbrt_accuracy)."""
+    rng = np.random.default_rng(11)
+    worst = 0.0
+    for law, coef in (("darcy_weisbach", 0.05), ("chezy", 40.0), ("manning", 0.04), ("strickler", 25.0)):
+        gcf = oracle.friction_gcf(law, coef)
+        for _ in range(400):
+            hs, hst = 10 ** rng.uniform(-4, 0.5, 2)
+            hus, hvs, hup, hvp = rng.normal(size=4) * 0.5
+            dt = rng.uniform(0.01, 1.0)
+            a, b = oracle.friction(gcf, law, dt, hs, hus, hvs, hst, hup, hvp)
+            umag = np.sqrt(hus * hus + hvs * hvs) * (1.0 / hs)
+            k = (dt * gcf) * umag
+            if law in ("darcy_weisbach", "chezy"):
+                w = k / hst
+            else:
+                sg = oracle.icbrt(hst)
+                w = k * ((sg * sg) * (sg * sg))
+            for got, q in ((a, hup), (b, hvp)):
+                want = q / (1.0 + w)             # the printed division
+                ulp = np.spacing(abs(want))
+                assert abs(got - want) <= 2 * ulp, (law, got, want)
+                worst = max(worst, abs(got - want) / ulp)
+    assert worst <= 2
+
+
 # ---------------------------------------------------------------- icbrt (Q20)
 def test_icbrt_accuracy():
     getcontext().prec = 50
