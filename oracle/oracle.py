@@ -15,6 +15,7 @@ _HERE = Path(__file__).resolve().parent
 _SRC = _HERE / "swof_oracle.c"
 _HDR = _HERE / "swof_oracle.h"
 _LIB = _HERE / "liboracle.so"
+_LIB_OMP = _HERE / "liboracle_omp.so"      # OpenMP-over-rows build (bitwise identical; development aid)
 # -ffp-contract=off: no FMA contraction; no -march=native, no -ffast-math (IEEE div/sqrt)
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
@@ -53,25 +54,37 @@ class Counters(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-def build(force: bool = False) -> Path:
-    """Compile liboracle.so with gcc (building the checker is not using it)."""
-    if not force and _LIB.exists() and _LIB.stat().st_mtime >= max(_SRC.stat().st_mtime, _HDR.stat().st_mtime):
-        return _LIB
-    tmp = _LIB.with_suffix(f".so.tmp{os.getpid()}")
-    subprocess.run(["gcc", *CFLAGS, "-o", str(tmp), str(_SRC), "-lm"], check=True)
-    os.replace(tmp, _LIB)
-    return _LIB
+def build(force: bool = False, omp: bool = False) -> Path:
+    """Compile liboracle.so (or, omp=True, liboracle_omp.so with -fopenmp) with gcc (building the checker is
+    not using it)."""
+    out = _LIB_OMP if omp else _LIB
+    if not force and out.exists() and out.stat().st_mtime >= max(_SRC.stat().st_mtime, _HDR.stat().st_mtime):
+        return out
+    tmp = out.with_suffix(f".so.tmp{os.getpid()}")
+    subprocess.run(["gcc", *CFLAGS, *(["-fopenmp"] if omp else []), "-o", str(tmp), str(_SRC), "-lm"], check=True)
+    os.replace(tmp, out)
+    return out
 
 
 _lib = None
+_lib_omp = None
 _D = C.POINTER(C.c_double)
 
 
-def lib():
-    global _lib
+def lib(omp: bool = False):
+    """The oracle library; omp=True: the OpenMP-over-rows build (same results bit for bit)."""
+    global _lib, _lib_omp
+    if omp:
+        if _lib_omp is None:
+            _lib_omp = _declare(C.CDLL(str(build(omp=True))))
+        return _lib_omp
     if _lib is None:
-        build()
-        L = C.CDLL(str(_LIB))
+        _lib = _declare(C.CDLL(str(build())))
+    return _lib
+
+
+def _declare(L):
+    if True:
         P = C.POINTER(OrParams)
         L.or_minmod.restype = C.c_double
         L.or_minmod.argtypes = [C.c_double, C.c_double]
@@ -114,8 +127,7 @@ def lib():
         L.or_flow_direction_f32.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         L.or_pairwise_sum.restype = C.c_double
         L.or_pairwise_sum.argtypes = [_D, C.c_int64]
-        _lib = L
-    return _lib
+    return L
 
 
 def _p(a):
@@ -277,8 +289,9 @@ def heun_step(P, z, fric, h, hu, hv, v, t, dt):
 
 
 def run(cfg_or_P, z=None, fric=None, h=None, hu=None, hv=None, v=None, t0=0.0, nsteps=None,
-        t_end=float("inf"), dt_forced=0.0):
-    """Run the oracle time loop.  Accepts a workloads.SwofConfig (inputs taken from it) or OrParams."""
+        t_end=float("inf"), dt_forced=0.0, omp=False):
+    """Run the oracle time loop.  Accepts a workloads.SwofConfig (inputs taken from it) or OrParams.
+    omp=True runs the OpenMP-over-rows build (bitwise identical state; counters summed in another order)."""
     if isinstance(cfg_or_P, OrParams):
         P = cfg_or_P
     else:
@@ -302,7 +315,7 @@ def run(cfg_or_P, z=None, fric=None, h=None, hu=None, hv=None, v=None, t0=0.0, n
     t = C.c_double(t0)
     done = C.c_int64()
     cnt = Counters()
-    rc = lib().or_run(C.byref(P), _p(_arr(z)), _p(_arr(fric) if fric is not None else None),
+    rc = lib(omp).or_run(C.byref(P), _p(_arr(z)), _p(_arr(fric) if fric is not None else None),
                       _p(h), _p(hu), _p(hv), _p(v), C.byref(t), int(nsteps), t_end, dt_forced,
                       _p(dth), cap, C.byref(done), C.byref(cnt))
     return {"rc": rc, "h": h, "hu": hu, "hv": hv, "v": v, "t": t.value, "steps": done.value,

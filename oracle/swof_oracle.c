@@ -16,6 +16,24 @@
 
 #define GH 2 /* ghost width = scheme order */
 
+/* Optional OpenMP-over-rows build (liboracle_omp.so, gcc -fopenmp; development aid for the full-size
+ * digests of tools/oracle_digests.py): the outer row loops of the whole-array passes run in parallel.
+ * Every element is still computed by the same expression from the same inputs, so the state is bitwise
+ * identical to the serial build (tests/test_oracle_omp.py); only the order of the diagnostic counter
+ * sums differs.  The default liboracle.so is built without -fopenmp: these pragmas are then inert. */
+#ifdef _OPENMP
+#define OR_PAR_FOR _Pragma("omp parallel for schedule(static)")
+#define OR_PAR_FOR_RED(...) _Pragma(OR_STR(omp parallel for schedule(static) reduction(__VA_ARGS__)))
+#define OR_PAR_FOR_SCHEME \
+    _Pragma("omp parallel for schedule(static) reduction(+ : n_clamps, n_capped, n_cells, cl_mass) reduction(max : cl_max)")
+#else
+#define OR_PAR_FOR_SCHEME
+#define OR_PAR_FOR
+#define OR_PAR_FOR_RED(...)
+#endif
+#define OR_STR2(x) #x
+#define OR_STR(x) OR_STR2(x)
+
 static double dmin(double a, double b) { return (a < b) ? a : b; }
 static double dmax(double a, double b) { return (a > b) ? a : b; }
 
@@ -392,6 +410,7 @@ static void fill_ghosts(const or_params* P, ws_t* W, double t_s) {
  * primitives on every cell incl. ghosts: rh = 1/h on wet cells (h > h_eps, Q6) else 0, u = hu rh,
  * v = hv rh, eta = h + z; then MUSCL per axis on cells -1 .. n (ghost layer 0 included). */
 static void primitives(const or_params* P, ws_t* W) {
+    OR_PAR_FOR
     for (int j = -GH; j < W->ny + GH; ++j)
         for (int i = -GH; i < W->nx + GH; ++i) {
             size_t c = PIX(W, i, j);
@@ -412,6 +431,7 @@ static void muscl_axis(ws_t* W, int axis, int order) {
     ptrdiff_t st = axis == 0 ? 1 : W->pw;
     const double* un = axis == 0 ? W->u : W->v;
     const double* ut = axis == 0 ? W->v : W->u;
+    OR_PAR_FOR
     for (int j = j0; j < j1; ++j)
         for (int i = i0; i < i1; ++i) {
             size_t c = PIX(W, i, j);
@@ -443,6 +463,7 @@ static void hydrostatic_axis(ws_t* W, int axis) {
     double* ZS = axis == 0 ? W->fx_zs : W->fy_zs;
     double* HL = axis == 0 ? W->fx_HL : W->fy_HL;
     double* HR = axis == 0 ? W->fx_HR : W->fy_HR;
+    OR_PAR_FOR
     for (int row = 0; row < nr; ++row)
         for (int f = 0; f < nf; ++f) {
             double l[5], r[5];
@@ -463,6 +484,8 @@ static void flux_axis(const or_params* P, ws_t* W, int axis, or_counters* C) {
     double* Ft = axis == 0 ? W->fx_Ft : W->fy_Ft;
     double* SL = axis == 0 ? W->fx_SL : W->fy_SL;
     double* SR = axis == 0 ? W->fx_SR : W->fy_SR;
+    long long n_dry = 0, n_left = 0, n_right = 0, n_mid = 0;
+    OR_PAR_FOR_RED(+ : n_dry, n_left, n_right, n_mid)
     for (int row = 0; row < nr; ++row)
         for (int f = 0; f < nf; ++f) {
             double l[5], r[5], F[3], c1, c2;
@@ -473,13 +496,17 @@ static void flux_axis(const or_params* P, ws_t* W, int axis, or_counters* C) {
                          : hll(P->g, P->h_eps, HL[k], l[3], l[4], HR[k], r[3], r[4], F, &c1, &c2);
             iface_sources(P->g, l[0], HL[k], r[0], HR[k], &SL[k], &SR[k]);
             Fm[k] = F[0]; Fn[k] = F[1]; Ft[k] = F[2];
-            if (C) {
-                if (br == 0) C->face_dry++;
-                else if (br == 1) C->face_left++;
-                else if (br == 2) C->face_right++;
-                else C->face_mid++;
-            }
+            if (br == 0) n_dry++;
+            else if (br == 1) n_left++;
+            else if (br == 2) n_right++;
+            else n_mid++;
         }
+    if (C) {
+        C->face_dry += n_dry;
+        C->face_left += n_left;
+        C->face_right += n_right;
+        C->face_mid += n_mid;
+    }
 }
 
 /* ---- Algorithm 1 step "Scheme computation" ----
@@ -491,6 +518,9 @@ static void scheme(const or_params* P, ws_t* W, const double* v_in, double t_s, 
     int nx = W->nx, ny = W->ny;
     double lx = dt / P->dx, ly = dt / P->dy;
     double Rdt = or_rain_rate(P, t_s) * dt;
+    long long n_clamps = 0, n_capped = 0, n_cells = 0;
+    double cl_mass = 0.0, cl_max = C ? C->clamp_max : 0.0;
+    OR_PAR_FOR_SCHEME
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
             size_t c = PIX(W, i, j);
@@ -511,11 +541,9 @@ static void scheme(const or_params* P, ws_t* W, const double* v_in, double t_s, 
             double hu1 = W->hu[c] - (lx * Dnx + ly * Dty);
             double hv1 = W->hv[c] - (lx * Dtx + ly * Dny);
             if (h1 < 0.0) {
-                if (C) {
-                    C->clamps++;
-                    C->clamped_mass += -h1;
-                    if (-h1 > C->clamp_max) C->clamp_max = -h1;
-                }
+                n_clamps++;
+                cl_mass += -h1;
+                if (-h1 > cl_max) cl_max = -h1;
                 h1 = 0.0;
             }
             double hr = h1 + Rdt;
@@ -523,13 +551,20 @@ static void scheme(const or_params* P, ws_t* W, const double* v_in, double t_s, 
             if (P->ga_enabled) {
                 or_green_ampt(P, hr, v_in[ic], dt, &hst, &V);
                 v_out[ic] = V;
-                if (C && v_in[ic] != 0.0) C->ga_capped++;
+                if (v_in[ic] != 0.0) n_capped++;
             }
             W->hs[ic] = hst;
             W->hup[ic] = hu1;
             W->hvp[ic] = hv1;
-            if (C) C->cell_stage++;
+            n_cells++;
         }
+    if (C) {
+        C->clamps += n_clamps;
+        C->clamped_mass += cl_mass;
+        C->clamp_max = cl_max;
+        C->ga_capped += n_capped;
+        C->cell_stage += n_cells;
+    }
 }
 
 /* ---- Algorithm 1 step "Frictions" ---- */
@@ -538,19 +573,23 @@ static void frictions(const or_params* P, ws_t* W, const double* fric, const dou
                       double* h_out, double* hu_out, double* hv_out, or_counters* C) {
     size_t n = (size_t)W->nx * W->ny;
     double gcf0 = or_friction_gcf(P->fric_law, P->fric_coef, P->g);
+    long long n_wet = 0;
+    OR_PAR_FOR_RED(+ : n_wet)
     for (size_t c = 0; c < n; ++c) {
         double gcf = fric ? or_friction_gcf(P->fric_law, fric[c], P->g) : gcf0;
         double hu, hv;
         or_friction(gcf, P->fric_law, P->h_eps, dt, h_in[c], hu_in[c], hv_in[c],
                     W->hs[c], W->hup[c], W->hvp[c], &hu, &hv);
-        if (C && W->hs[c] > P->h_eps && P->fric_law != OR_FRIC_NONE) C->cell_wet_fric++;
+        if (W->hs[c] > P->h_eps && P->fric_law != OR_FRIC_NONE) n_wet++;
         h_out[c] = W->hs[c];
         hu_out[c] = hu;
         hv_out[c] = hv;
     }
+    if (C) C->cell_wet_fric += n_wet;
 }
 
 static void load_padded(ws_t* W, const double* z, const double* h, const double* hu, const double* hv) {
+    OR_PAR_FOR
     for (int j = 0; j < W->ny; ++j)
         for (int i = 0; i < W->nx; ++i) {
             size_t c = PIX(W, i, j), s = (size_t)j * W->nx + i;
@@ -595,6 +634,7 @@ static void heun_ws(const or_params* P, ws_t* W, const double* z, const double* 
     stage_ws(P, W, z, fric, h, hu, hv, v, t, dt, W->U1h, W->U1hu, W->U1hv, W->U1v, C);
     stage_ws(P, W, z, fric, W->U1h, W->U1hu, W->U1hv, W->U1v, t + dt, dt,
              W->U2h, W->U2hu, W->U2hv, W->U2v, C);
+    OR_PAR_FOR
     for (size_t c = 0; c < n; ++c) {
         h[c] = 0.5 * (h[c] + W->U2h[c]);
         hu[c] = 0.5 * (hu[c] + W->U2hu[c]);
@@ -608,6 +648,7 @@ static void euler_ws(const or_params* P, ws_t* W, const double* z, const double*
                      double* h, double* hu, double* hv, double* v, double t, double dt, or_counters* C) {
     size_t n = (size_t)P->nx * P->ny;
     stage_ws(P, W, z, fric, h, hu, hv, v, t, dt, W->U1h, W->U1hu, W->U1hv, W->U1v, C);
+    OR_PAR_FOR
     for (size_t c = 0; c < n; ++c) {
         h[c] = W->U1h[c];
         hu[c] = W->U1hu[c];

@@ -1,0 +1,76 @@
+"""Full-size, full-step-count oracle results of BASELINE.json's configurations, stored as digests.
+
+Writes tests/golden/full_size_digests.json (calls only oracle/ and workloads/; no value comes from the CUDA
+path).  For each configuration at its full size the oracle (the OpenMP-over-rows build, bitwise identical to
+the serial one: tests/test_oracle_omp.py) runs the configuration's whole horizon (Algorithm 1's time loop,
+PAPER.md P:773-788) and the file records SHA-256 digests of the final h, hu, hv, V rasters (float64, row-major)
+and of the dt sequence, plus summary values for diagnosis.  tests/test_gpu_full_size.py runs the GPU path on
+the same inputs and compares digests: equal digests mean the GPU state equals the oracle's bit for bit
+(hence within every north_star tolerance, masks and dt sequence included).
+
+    OMP_NUM_THREADS=7 python tools/oracle_digests.py cfg1 cfg2 cfg4 cfg3
+
+Run time on 8 host cores: cfg1 ~7 min, cfg2 ~15 min, cfg4 ~4 h, cfg3 ~5 h (cfg4 needs ~36 GB of RAM).
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import oracle  # noqa: E402
+from workloads import make  # noqa: E402
+
+OUT = ROOT / "tests" / "golden" / "full_size_digests.json"
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def source_digest() -> str:
+    """The oracle's arithmetic and the input generator: digests are stale if either changes."""
+    h = hashlib.sha256()
+    for p in ("oracle/swof_oracle.c", "oracle/swof_oracle.h", "workloads/configs.py", "workloads/rng.py",
+              "workloads/dem.py"):
+        h.update((ROOT / p).read_bytes())
+    return h.hexdigest()
+
+
+def main(names):
+    data = json.loads(OUT.read_text()) if OUT.exists() else {}
+    data["_source"] = ("tools/oracle_digests.py: oracle (OpenMP-over-rows build, bitwise = serial) at each "
+                       "configuration's full size and full step count; SHA-256 of the float64 rasters")
+    src = source_digest()
+    for name in names:
+        cfg = make(name)
+        t0 = time.time()
+        r = oracle.run(cfg, omp=True)
+        el = time.time() - t0
+        assert r["rc"] == 0, r["rc"]
+        h = r["h"]
+        ent = {
+            "nx": cfg.nx, "ny": cfg.ny, "steps": int(r["steps"]), "t": r["t"], "t_end": cfg.t_end,
+            "sha_h": sha(h), "sha_hu": sha(r["hu"]), "sha_hv": sha(r["hv"]),
+            "sha_v": sha(r["v"]) if r["v"] is not None else None,
+            "sha_dt": sha(r["dt"]), "dt_first": float(r["dt"][0]), "dt_last": float(r["dt"][-1]),
+            "wet": int(np.count_nonzero(h > cfg.h_eps)), "sum_h": float(oracle.pairwise_sum(h)),
+            "max_h": float(h.max()), "clamps": int(r["counters"].clamps),
+            "clamp_max": float(r["counters"].clamp_max), "source_sha": src,
+            "oracle_seconds": round(el, 1), "threads": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())),
+        }
+        data[name] = ent
+        OUT.write_text(json.dumps(data, indent=1) + "\n")
+        print(name, json.dumps(ent), flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["cfg1", "cfg2", "cfg4", "cfg3"])
