@@ -72,7 +72,10 @@ extern "C" {
 
 /* diagnostic flags */
 #define SWOF_FLAG_NONFINITE 1u  /* NaN/Inf in the CFL maximum -> stepping halted                 */
-#define SWOF_FLAG_BIGCLAMP 2u   /* a single negative-height clamp larger than params.clamp_fail  */
+#define SWOF_FLAG_BIGCLAMP 2u   /* a single negative-height clamp larger than params.clamp_fail
+                                   -> stepping halted: the step that raised it is not completed, so
+                                   the state stays that of the last completed step (SPEC's
+                                   NegativeHeight abort)                                   */
 #define SWOF_FLAG_BADINPUT 4u   /* set_state saw h < 0 or a non-finite value                     */
 
 typedef struct swof_params {
@@ -101,8 +104,12 @@ typedef struct swof_params {
     double hydro_q[4][SWOF_MAX_TABLE];  /* Q [m^3/s] over the segment; piecewise linear, clamped  */
     int64_t dt_hist_cap;     /* dt history capacity (0 -> 1<<20 steps)                             */
     int32_t graph_steps;     /* Heun steps per captured CUDA graph (0 -> 16; rounded up to even)  */
-    double clamp_fail;       /* a single negative-height clamp above this [m] raises SWOF_FLAG_BIGCLAMP
-                                and SWOF_ENUMERIC (0 -> 1e-6 m; DESIGN.md §3 Q17)                  */
+    double clamp_fail;       /* a single negative-height clamp above this [m] raises SWOF_FLAG_BIGCLAMP,
+                                halts stepping and returns SWOF_ENUMERIC.  0 -> 1e-6 m, not SURVEY
+                                §8b's 1e-10 m: full-size cfg4 clamps 2.28e-10 m in step 0, a
+                                film the cell-centred CFL of U^n does not bound, reproduced bit for
+                                bit by the oracle (DESIGN.md §3 Q17); 1e-6 m is still a positivity
+                                failure, not round-off                                             */
     int32_t flux;            /* SWOF_FLUX_*                                                       */
     int32_t order;           /* 2 (or 0): MUSCL + Heun; 1: first order in
                                 space (no reconstruction) and explicit Euler in time      */
@@ -155,12 +162,14 @@ int swof_set_state(swof_ctx* c, const double* h, const double* hu, const double*
                    double t0);
 
 /* Advance nsteps time steps (Heun, or explicit Euler at order 1) with dt = min(CFL dt, dt_max) each
- * (no t_end clipping).
- * Returns SWOF_ENUMERIC if a flag is set afterwards. */
+ * (no t_end clipping).  A halt flag stops stepping at the last completed step (the remaining steps are
+ * device-side no-ops).  Returns SWOF_ENUMERIC if a flag is set afterwards. */
 int swof_step(swof_ctx* c, int64_t nsteps);
 
 /* Advance until t >= t_end or max_steps steps were taken; the last dt is clipped so that t lands on
- * t_end exactly.  steps_done (nullable) receives the number of steps taken by this call. */
+ * t_end exactly.  steps_done (nullable) receives the number of steps taken by this call.  max_steps is
+ * counted from the current step and saturates (INT64_MAX = no cap).  A halt flag (non-finite CFL
+ * maximum, a clamp above clamp_fail) stops the run at the last completed step: SWOF_ENUMERIC. */
 int swof_run(swof_ctx* c, double t_end, int64_t max_steps, int64_t* steps_done);
 
 /* Copy the state out (host or device pointers; any of the arrays may be NULL; v_inf is left

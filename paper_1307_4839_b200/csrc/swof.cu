@@ -16,11 +16,10 @@
 #include "../../include/swof.h"
 #include "swof_kernels.cuh"
 #include "swof_d8.cuh"
-#ifndef SWOF_MARCH
-#define SWOF_MARCH 1                   // 1: the register-marching stage kernel (swof_march.cuh) by default
-#endif
-#if SWOF_MARCH
 #include "swof_march.cuh"
+#include "swof_march2.cuh"
+#ifndef SWOF_PAIR
+#define SWOF_PAIR 0                    // 1: two columns per lane (swof_march2.cuh); 0: one (swof_march.cuh)
 #endif
 
 using namespace swof;
@@ -40,7 +39,6 @@ struct swof_ctx {
     DevState* h_st = nullptr;          // pinned mirror of the device scalar state
     double* d_part = nullptr;          // diag partials
     int diag_blocks = 0;
-    dim3 grid;
     StageFn kpred = nullptr, kcorr = nullptr;   // stage kernel instances for this context's physics
     dim3 cf_grid;                               // face-CFL pass tiles
     dim3 sgrid, sblock;                         // stage kernel launch shape
@@ -275,27 +273,32 @@ int swof_workspace_size(const swof_params* p, size_t* bytes) {
     return SWOF_OK;
 }
 
-// Picks the stage kernels for the context's physics and options and their launch shape: the marching
-// kernel (swof_march.cuh); the tiled stage_kernel in SWOF_MARCH=0 builds.
+// Picks the stage kernels (swof_march.cuh) for the context's physics and options and their launch shape.
 static int choose_kernels(swof_ctx* c) {
     const KParams& k = c->kp;
     const bool ff = c->kb.fric != nullptr;
     const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
     const bool push = c->kb.push_any != 0, dry = c->p.dry_skip != 0;
-#if SWOF_MARCH
     {
+#if SWOF_PAIR
+        c->kpred = select_march2<false>(k.fk, k.ga != 0, ff, generic, push, dry);
+        c->kcorr = select_march2<true>(k.fk, k.ga != 0, ff, generic, push, dry);
+        const int own_cols = M2_OWN, nw = 1;
+#else
         c->kpred = select_march<false>(k.fk, k.ga != 0, ff, generic, push, dry);
         c->kcorr = select_march<true>(k.fk, k.ga != 0, ff, generic, push, dry);
+        const int own_cols = M_OWN, nw = M_NW;
+#endif
         // rows per warp segment, 1..64: minimise (waves of segments over the resident warp slots) x (rows +
         // ~3 rows of halo work per segment) -- small grids get short segments to fill the 148 SMs
         int occ_p = 0, occ_c = 0, dev = 0, nsm = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, c->kpred, M_NW * 32, 0);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, c->kcorr, M_NW * 32, 0);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, c->kpred, nw * 32, 0);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, c->kcorr, nw * 32, 0);
         if (e == cudaSuccess) e = cudaGetDevice(&dev);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return cuda_fail(c, e, "march kernel occupancy");
-        const long long slots = (long long)(occ_p < occ_c ? occ_p : occ_c) * nsm * M_NW;
-        const long long nstrip = (k.nx + M_OWN - 1) / M_OWN;
+        const long long slots = (long long)(occ_p < occ_c ? occ_p : occ_c) * nsm * nw;
+        const long long nstrip = (k.nx + own_cols - 1) / own_cols;
         int mh = 64;
         double best = 1e300;
         for (int h = 1; h <= 64; ++h) {
@@ -324,21 +327,11 @@ static int choose_kernels(swof_ctx* c) {
         c->kp.march_h2 = h2;
         const long long nseg = g1 + (k.ny - (long long)g1 * mh + h2 - 1) / h2;
         const long long nwarps = nstrip * (k.ny > (long long)g1 * mh ? nseg : g1);
-        c->sgrid = dim3((unsigned)((nwarps + M_NW - 1) / M_NW));
-        c->sblock = dim3(M_NW * 32);
+        c->sgrid = dim3((unsigned)((nwarps + nw - 1) / nw));
+        c->sblock = dim3(nw * 32);
         c->ssmem = 0;
         return SWOF_OK;
     }
-#endif
-    c->kpred = select_stage<false>(k.fk, k.ga != 0, ff, generic, push, dry);
-    c->kcorr = select_stage<true>(k.fk, k.ga != 0, ff, generic, push, dry);
-    cudaError_t e = cudaFuncSetAttribute(c->kpred, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(c->kcorr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(c, e, "stage kernel attributes");
-    c->sgrid = c->grid;
-    c->sblock = dim3(NT);
-    c->ssmem = SMEM_BYTES;
-    return SWOF_OK;
 }
 
 int swof_create(const swof_params* p, const double* z, const double* fric_field, void* d_workspace, size_t ws_bytes,
@@ -406,7 +399,6 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
                    : (double)(p->inflow_k1[s] - p->inflow_k0[s]) * ((s < 2) ? p->dy : p->dx);
         for (int i = 0; i < k.n_hydro[s]; ++i) { k.hydro_t[s][i] = p->hydro_t[s][i]; k.hydro_q[s][i] = p->hydro_q[s][i]; }
     }
-    c->grid = dim3((unsigned)((p->nx + TX - 1) / TX), (unsigned)((p->ny + TY - 1) / TY));
     c->diag_blocks = DIAG_BLOCKS;
     c->cf_grid = dim3((unsigned)((p->nx + CF_TX - 1) / CF_TX), (unsigned)((p->ny + CF_TY - 1) / CF_TY));
 
@@ -415,13 +407,6 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
         if (rc != SWOF_OK) { swof_destroy(c); return rc; }
     }
     cudaError_t e = cudaSuccess;
-    {   // resident CTAs of the tiled stage kernel: the distance of its (off by default) next-tile L2 prefetch
-        int per_sm = 0, dev = 0, sms = 0;
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_stage<false>(k.fk, k.ga != 0, has_ff, true, false, false), NT, SMEM_BYTES);
-        if (e == cudaSuccess) e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        k.pf_stride = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 1);
-    }
     if (e == cudaSuccess) e = cudaMemsetAsync(c->ws, 0, L.total, c->stream);
     if (e != cudaSuccess) { int rc = cuda_fail(c, e, "swof_create"); fprintf(stderr, "swof: %s\n", c->err.c_str()); swof_destroy(c); return rc; }
     int rc = copy_field_in(c, b.z, z);
@@ -497,7 +482,8 @@ int swof_run(swof_ctx* c, double t_end, int64_t max_steps, int64_t* steps_done) 
     int rc;
     if ((rc = read_state(c))) return rc;
     const long long step0 = c->h_st->step[c->par];
-    const long long lim = step0 + max_steps;
+    // saturating: max_steps = INT64_MAX means 'no cap' whatever the steps already taken
+    const long long lim = (max_steps > INT64_MAX - step0) ? (long long)INT64_MAX : step0 + max_steps;
     CK(cudaMemcpyAsync(&c->kb.st->t_end, &t_end, sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(&c->kb.st->step_limit, &lim, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
     // replay until the device reports done (t >= t_end, step limit, or a halt); steps past the end
@@ -506,7 +492,7 @@ int swof_run(swof_ctx* c, double t_end, int64_t max_steps, int64_t* steps_done) 
     for (;;) {
         const long long cur = c->h_st->step[c->par];
         const double tc = c->h_st->t[c->par];
-        if (!(tc < t_end) || cur >= lim || (c->h_st->flags & FLAG_NONFINITE)) break;
+        if (!(tc < t_end) || cur >= lim || (c->h_st->flags & (FLAG_NONFINITE | FLAG_BIGCLAMP))) break;
         int64_t left = lim - cur;
         int64_t n = left < batch ? left : batch;
         if ((rc = enqueue_steps(c, n))) return rc;

@@ -20,7 +20,9 @@ constexpr int M_OWN = 28;              // own columns per warp
 #ifndef SWOF_MARCH_VOTE
 #define SWOF_MARCH_VOTE 1
 #endif
-#if SWOF_MARCH_VOTE
+#if SWOF_TOL || SWOF_NOVOTE
+#define M_SLOW(...) ((void)(__VA_ARGS__), false)
+#elif SWOF_MARCH_VOTE
 #define M_SLOW(...) __any_sync(0xffffffffu, (__VA_ARGS__))
 #else
 #define M_SLOW(...) (__VA_ARGS__)
@@ -40,6 +42,7 @@ constexpr int M_NW = SWOF_MARCH_NW;    // warps per CTA (independent); rows per 
 #endif
 
 struct MPrim { double h, e, u, v, rh; };
+using StageFn = void (*)(KParams, KBufs, int);
 
 // rows [j0, jend) of segment row g: march_h rows high, the last wave's segments march_h2 rows high
 __device__ __forceinline__ void march_seg(const KParams& P, int g, int& j0, int& jend) {
@@ -155,7 +158,8 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         const double ax = u2d(st->amax[par][0]), ay = u2d(st->amax[par][1]);
         const double t_end = st->t_end;
         const bool finite = isfinite(ax) && isfinite(ay);
-        const bool done = !(t < t_end) || step >= st->step_limit || !finite;
+        // halt: past t_end, at the step limit, a non-finite CFL maximum, or a clamp above clamp_fail
+        const bool done = !(t < t_end) || step >= st->step_limit || !finite || (st->flags & FLAG_BIGCLAMP) != 0;
         if (leader) {
             if (done) {
                 if (!CORRECTOR) {

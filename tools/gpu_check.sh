@@ -10,7 +10,7 @@ bench) timeout 900 python bench.py --steps 50 --warmup 5 > gpurun_out/bench.log 
 ncu)
 CMD="python bench.py --nx 4096 --ny 4096 --steps 4 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"stage_kernel|march_kernel" -s 6 -c 2 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"march_kernel" -s 6 -c 2 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_full.log ;;
 launches)
 CMD="python bench.py --nx 4096 --ny 4096 --steps 4 --warmup 3 --no-cpu-baseline"
@@ -26,7 +26,7 @@ ncu8k)
 CMD="python bench.py --steps 4 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain8k.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches8k.csv $CMD > gpurun_out/ncu_list8k.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"stage_kernel|march_kernel" -s 6 -c 2 -o gpurun_out/prof8k $CMD > gpurun_out/ncu_full8k.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"march_kernel" -s 6 -c 2 -o gpurun_out/prof8k $CMD > gpurun_out/ncu_full8k.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_full8k.log ;;
 esac
 done

@@ -15,7 +15,7 @@ for v in "$@"; do
   fi
   cp paper_1307_4839_b200/libswof.so gpurun_out/libswof_nv$i.so
   $CMD > gpurun_out/plain_nv$i.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"stage_kernel|march_kernel" -s 6 -c 2 -o gpurun_out/prof_nv$i $CMD > gpurun_out/ncu_nv$i.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"march_kernel" -s 6 -c 2 -o gpurun_out/prof_nv$i $CMD > gpurun_out/ncu_nv$i.log 2>&1
   echo "$i $v rc=$?" >> gpurun_out/ncu_variants.log
 done
 python -m paper_1307_4839_b200.build --force > /dev/null 2>&1

@@ -8,8 +8,8 @@ import tempfile
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-pat = sys.argv[1] if len(sys.argv) > 1 else "stage_kernelILb0ENS_4PhysILi1ELb1ELb0E"
-src = (ROOT / "paper_1307_4839_b200/csrc/swof_kernels.cuh").read_text().split("\n")
+pat = sys.argv[1] if len(sys.argv) > 1 else "march_kernelILb0ENS_4PhysILi1ELb1ELb0E"
+src = (ROOT / "paper_1307_4839_b200/csrc/swof_march.cuh").read_text().split("\n")
 kstart = next(i for i, l in enumerate(src) if "__global__ void __launch_bounds__" in l) + 1
 kend = next(i for i in range(kstart, len(src)) if src[i].startswith("}")) + 1
 with tempfile.TemporaryDirectory() as d:
@@ -26,7 +26,7 @@ for l in dis.split("\n"):
         continue
     if func is None or pat not in func:
         continue
-    if "## File" in l and "swof_kernels.cuh" in l:
+    if "## File" in l and "swof_march.cuh" in l:
         nums = [int(x) for x in re.findall(r"line (\d+)", l)]
         body = [n for n in nums if kstart <= n <= kend]
         cur = body[-1] if body else (nums[0] if nums else None)
