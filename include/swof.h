@@ -172,15 +172,17 @@ int swof_step(swof_ctx* c, int64_t nsteps);
  * maximum, a clamp above clamp_fail) stops the run at the last completed step: SWOF_ENUMERIC. */
 int swof_run(swof_ctx* c, double t_end, int64_t max_steps, int64_t* steps_done);
 
-/* Copy the state out (host or device pointers; any of the arrays may be NULL; v_inf is left
+/* The three getters take a const context: the state is not changed (they use the context's stream,
+ * its diagnostics scratch and its last-error text).
+ * Copy the state out (host or device pointers; any of the arrays may be NULL; v_inf is left
  * untouched when Green-Ampt is off).  t and step (nullable) receive the simulated time and count. */
-int swof_get_state(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf, double* t, int64_t* step);
+int swof_get_state(const swof_ctx* c, double* h, double* hu, double* hv, double* v_inf, double* t, int64_t* step);
 
 /* Copy min(cap, steps taken) entries of the dt history (host pointer); n receives that count. */
-int swof_get_dt_history(swof_ctx* c, double* dt, int64_t cap, int64_t* n);
+int swof_get_dt_history(const swof_ctx* c, double* dt, int64_t cap, int64_t* n);
 
 /* Fixed-order diagnostics of the current state (not part of the time loop). */
-int swof_get_diag(swof_ctx* c, swof_diag* d);
+int swof_get_diag(const swof_ctx* c, swof_diag* d);
 
 /* Testing/profiling entry points (same kernels as swof_step):
  * swof_predictor: run only the predictor stage U* = S(U^n; t^n) of the next step and copy U*, V*

@@ -503,7 +503,8 @@ int swof_run(swof_ctx* c, double t_end, int64_t max_steps, int64_t* steps_done) 
     return flags_rc(c);
 }
 
-int swof_get_state(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf, double* t, int64_t* step) {
+int swof_get_state(const swof_ctx* cc, double* h, double* hu, double* hv, double* v_inf, double* t, int64_t* step) {
+    swof_ctx* c = const_cast<swof_ctx*>(cc);  // logically const: only scratch, the state cache and err change
     if (!c) return SWOF_EINVAL;
     if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_get_state before swof_set_state");
     int rc;
@@ -517,7 +518,8 @@ int swof_get_state(swof_ctx* c, double* h, double* hu, double* hv, double* v_inf
     return SWOF_OK;
 }
 
-int swof_get_dt_history(swof_ctx* c, double* dt, int64_t cap, int64_t* n) {
+int swof_get_dt_history(const swof_ctx* cc, double* dt, int64_t cap, int64_t* n) {
+    swof_ctx* c = const_cast<swof_ctx*>(cc);  // logically const: only scratch, the state cache and err change
     if (!c || (!dt && cap > 0) || cap < 0) return SWOF_EINVAL;
     if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_get_dt_history before swof_set_state");
     int rc;
@@ -533,7 +535,8 @@ int swof_get_dt_history(swof_ctx* c, double* dt, int64_t cap, int64_t* n) {
     return SWOF_OK;
 }
 
-int swof_get_diag(swof_ctx* c, swof_diag* d) {
+int swof_get_diag(const swof_ctx* cc, swof_diag* d) {
+    swof_ctx* c = const_cast<swof_ctx*>(cc);  // logically const: only scratch, the state cache and err change
     if (!c || !d) return SWOF_EINVAL;
     if (!c->have_state) return fail(c, SWOF_ESTATE, "swof_get_diag before swof_set_state");
     diag_kernel<<<c->diag_blocks, DIAG_NT, 0, c->stream>>>(c->kp, c->kb, c->d_part);

@@ -65,7 +65,7 @@ def test_one_step(gpu, name, nx, ny):
     print(name, res)
 
 
-FULL = [("cfg0", 64, 64, None), ("cfg1", 100, 70, None), ("cfg2", 97, 53, None), ("cfg3", 130, 90, 1500),
+FULL = [("cfg0", 64, 64, None), ("cfg1", 100, 70, None), ("cfg2", 97, 53, None), ("cfg3", 130, 90, None),
         ("cfg4", 75, 41, None)]
 
 

@@ -20,6 +20,10 @@ VARIANTS = {
     "darcyga": dict(ga_form="darcy"),
     "all": dict(flux="rusanov", order=1, cfl=1.0, cfl_mode="face", ga_form="darcy"),
     "dryskip": dict(dry_skip=True),          # GPU-only optimisation: results must not change
+    # the other two friction laws of P:80-90 (C_f = 1/K^2 and 1/C^2); on cfg3 the per-cell field becomes
+    # K = 1/n (resp. C = 1/n), so the kernels' per-cell branches of both laws run too
+    "strickler": dict(fric_law="strickler", fric_coef=25.0),
+    "chezy": dict(fric_law="chezy", fric_coef=40.0),
 }
 CASES = [("cfg0", 64, 64), ("cfg1", 100, 70), ("cfg3", 130, 90), ("cfg4", 75, 41)]
 
@@ -29,6 +33,8 @@ def variant_cfg(name, nx, ny, kw, steps):
     cfg.steps, cfg.t_end = steps, None
     for k, v in kw.items():
         setattr(cfg, k, v)
+    if kw.get("fric_law") in ("strickler", "chezy") and cfg.fric_field is not None:
+        cfg.fric_field = np.ascontiguousarray(1.0 / cfg.fric_field)
     if name == "cfg3":
         # the dry valley has no CFL speed, so step 0 takes dt = dt_max = 1 s while the critical inflow
         # ghost (Q18) pours in; the variants' corrector then clamps centimetres (both sides alike,

@@ -4,7 +4,10 @@ Writes tests/golden/full_size_digests.json (calls only oracle/ and workloads/; n
 path).  For each configuration at its full size the oracle (the OpenMP-over-rows build, bitwise identical to
 the serial one: tests/test_oracle_omp.py) runs the configuration's whole horizon (Algorithm 1's time loop,
 PAPER.md P:773-788) and the file records SHA-256 digests of the final h, hu, hv, V rasters (float64, row-major)
-and of the dt sequence, plus summary values for diagnosis.  tests/test_gpu_full_size.py runs the GPU path on
+and of the dt sequence, the SHA-256 of the packed wet mask (h > h_eps), plus summary values for diagnosis;
+tests/golden/full_size/<cfg>.npz holds the whole dt sequence and the final h, hu, hv, V at 4096 seeded sample
+cells (so that a GPU build that is not bitwise can still be held to the north_star tolerances: <= 1e-8 on the
+samples, the identical wet mask by its digest, dt to 1e-13).  tests/test_gpu_full_size.py runs the GPU path on
 the same inputs and compares digests: equal digests mean the GPU state equals the oracle's bit for bit
 (hence within every north_star tolerance, masks and dt sequence included).
 
@@ -30,6 +33,18 @@ import oracle  # noqa: E402
 from workloads import make  # noqa: E402
 
 OUT = ROOT / "tests" / "golden" / "full_size_digests.json"
+NPZ = ROOT / "tests" / "golden" / "full_size"
+N_SAMPLES = 4096
+
+
+def sample_index(name: str, ncell: int) -> np.ndarray:
+    """The sampled cells (flat row-major indices): a seeded draw, sorted, plus the first and last cell."""
+    rs = np.random.default_rng(int.from_bytes(hashlib.sha256(name.encode()).digest()[:8], "little"))
+    return np.unique(np.concatenate([[0, ncell - 1], rs.integers(0, ncell, N_SAMPLES - 2)]))
+
+
+def mask_sha(h, h_eps) -> str:
+    return hashlib.sha256(np.packbits(np.ascontiguousarray(h > h_eps)).tobytes()).hexdigest()
 
 
 def sha(a) -> str:
@@ -62,11 +77,17 @@ def main(names):
             "sha_h": sha(h), "sha_hu": sha(r["hu"]), "sha_hv": sha(r["hv"]),
             "sha_v": sha(r["v"]) if r["v"] is not None else None,
             "sha_dt": sha(r["dt"]), "dt_first": float(r["dt"][0]), "dt_last": float(r["dt"][-1]),
-            "wet": int(np.count_nonzero(h > cfg.h_eps)), "sum_h": float(oracle.pairwise_sum(h)),
+            "sha_mask": mask_sha(h, cfg.h_eps), "wet": int(np.count_nonzero(h > cfg.h_eps)), "sum_h": float(oracle.pairwise_sum(h)),
             "max_h": float(h.max()), "clamps": int(r["counters"].clamps),
             "clamp_max": float(r["counters"].clamp_max), "source_sha": src,
             "oracle_seconds": round(el, 1), "threads": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())),
         }
+        idx = sample_index(name, h.size)
+        NPZ.mkdir(parents=True, exist_ok=True)
+        np.savez_compressed(NPZ / f"{name}.npz", idx=idx, dt=r["dt"], h=h.ravel()[idx], hu=r["hu"].ravel()[idx],
+                            hv=r["hv"].ravel()[idx],
+                            v=(r["v"].ravel()[idx] if r["v"] is not None else np.zeros(0)))
+        data = json.loads(OUT.read_text()) if OUT.exists() else data  # other runs may have written meanwhile
         data[name] = ent
         OUT.write_text(json.dumps(data, indent=1) + "\n")
         print(name, json.dumps(ent), flush=True)
