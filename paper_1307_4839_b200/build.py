@@ -1,7 +1,10 @@
 """Build libswof.so (the C-ABI library, include/swof.h) in-tree for sm_100a with nvcc.
 
--fmad=false: no multiply-add contraction (the evaluation order is the canonical sheet of DESIGN.md §3);
-division and sqrt stay IEEE (nvcc defaults: -prec-div=true -prec-sqrt=true -ftz=false).
+libswof.so is the bit-identical build (-DSWOF_EXACT=1 -fmad=false): no multiply-add contraction, the
+evaluation order of every expression is the oracle's canonical sheet, division and sqrt IEEE
+(nvcc defaults: -prec-div=true -prec-sqrt=true -ftz=false).  tolerance=True builds the measured-and-rejected
+tolerance-contract variant (-DSWOF_EXACT=0 -fmad=true; DESIGN.md §3 "contract") into another file, for
+A/B experiments only.
 """
 from __future__ import annotations
 
@@ -21,28 +24,33 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
+    "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
     "-Xptxas", "-v",
     "-shared", "-Xcompiler", "-fPIC",
     "-I", str(ROOT / "include"),
 ]
 
 
-def stale() -> bool:
-    if not LIB.exists():
+def stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out: Path = LIB) -> Path:
-    """Compile the library (out: another file for a diagnostic build, e.g. -DSWOF_CHECK=1)."""
-    out = Path(out)
-    if out == LIB and not force and not stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path = None, tolerance: bool = False) -> Path:
+    """Compile the library (out: another file for a diagnostic build, e.g. -DSWOF_CHECK=1, or for the
+    tolerance=True experiment)."""
+    out = Path(out) if out is not None else LIB
+    if tolerance and out == LIB:
+        raise ValueError("the tolerance-contract variant is an experiment: build it into another file")
+    if out == LIB and not force and not stale(out):
+        return out
     tmp = out.with_suffix(f".so.tmp{os.getpid()}")
     extra = os.environ.get("SWOF_NVCC_EXTRA", "").split()        # A/B experiments (tools/ab.sh) only
-    cmd = [NVCC, *NVCC_FLAGS, *extra, *[f"-D{d}" for d in defines], "-o", str(tmp), *map(str, SOURCES), "-lcudart"]
+    mode = ["-DSWOF_EXACT=0", "-fmad=true"] if tolerance else ["-DSWOF_EXACT=1", "-fmad=false"]
+    cmd = [NVCC, *NVCC_FLAGS, *mode, *extra, *[f"-D{d}" for d in defines], "-o", str(tmp), *map(str, SOURCES),
+           "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -56,5 +64,5 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: Path = LI
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, defines=[a[2:] for a in sys.argv[1:] if a.startswith("-D")])
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True,
+                defines=[a[2:] for a in sys.argv[1:] if a.startswith("-D")]))

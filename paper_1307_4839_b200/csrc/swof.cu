@@ -17,10 +17,6 @@
 #include "swof_kernels.cuh"
 #include "swof_d8.cuh"
 #include "swof_march.cuh"
-#include "swof_march2.cuh"
-#ifndef SWOF_PAIR
-#define SWOF_PAIR 0                    // 1: two columns per lane (swof_march2.cuh); 0: one (swof_march.cuh)
-#endif
 
 using namespace swof;
 
@@ -280,15 +276,9 @@ static int choose_kernels(swof_ctx* c) {
     const bool generic = k.flux != SWOF_FLUX_HLL || k.order == 1 || k.ga_form != SWOF_GA_PRINTED;
     const bool push = c->kb.push_any != 0, dry = c->p.dry_skip != 0;
     {
-#if SWOF_PAIR
-        c->kpred = select_march2<false>(k.fk, k.ga != 0, ff, generic, push, dry);
-        c->kcorr = select_march2<true>(k.fk, k.ga != 0, ff, generic, push, dry);
-        const int own_cols = M2_OWN, nw = 1;
-#else
         c->kpred = select_march<false>(k.fk, k.ga != 0, ff, generic, push, dry);
         c->kcorr = select_march<true>(k.fk, k.ga != 0, ff, generic, push, dry);
         const int own_cols = M_OWN, nw = M_NW;
-#endif
         // rows per warp segment, 1..64: minimise (waves of segments over the resident warp slots) x (rows +
         // ~3 rows of halo work per segment) -- small grids get short segments to fill the 148 SMs
         int occ_p = 0, occ_c = 0, dev = 0, nsm = 0;

@@ -8,6 +8,7 @@
 // tiled stage_kernel of swof_kernels.cuh runs in SWOF_MARCH=0 builds.  DESIGN.md §5 has the design and
 // its measurements, §8 the rejected variants (their switches below stay off).
 #pragma once
+#include <type_traits>
 
 namespace swof {
 
@@ -20,8 +21,11 @@ constexpr int M_OWN = 28;              // own columns per warp
 #ifndef SWOF_MARCH_VOTE
 #define SWOF_MARCH_VOTE 1
 #endif
-#if SWOF_TOL || SWOF_NOVOTE
-#define M_SLOW(...) ((void)(__VA_ARGS__), false)
+#if !SWOF_EXACT
+// the tolerance build has no slow path, but keeps the warp vote (on a predicate that is never true): it closes
+// the scheduling region there -- one unbroken row body measured 11 % slower (ptxas interleaves the whole row
+// and runs short of registers at 168)
+#define M_SLOW(...) ((void)(__VA_ARGS__), __any_sync(0xffffffffu, m_never))
 #elif SWOF_MARCH_VOTE
 #define M_SLOW(...) __any_sync(0xffffffffu, (__VA_ARGS__))
 #else
@@ -42,6 +46,14 @@ constexpr int M_NW = SWOF_MARCH_NW;    // warps per CTA (independent); rows per 
 #endif
 
 struct MPrim { double h, e, u, v, rh; };
+
+// a global load issued at its program point (volatile asm is neither removed nor moved past other volatile
+// asm; the value is still scheduled like any register)
+__device__ __forceinline__ double ld_early(const double* p) {
+    double v;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
 using StageFn = void (*)(KParams, KBufs, int);
 
 // rows [j0, jend) of segment row g: march_h rows high, the last wave's segments march_h2 rows high
@@ -126,6 +138,8 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
     DevState* st = B.st;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool leader = blockIdx.x == 0 && tid == 0;
+    const bool m_never = P.nx < 0;     // never true (swof_create validates nx >= 1); see M_SLOW
+    (void)m_never;
 #if SWOF_MARCH_EARLY
     // interior warps issue the loads of their first three rows before the step scalars are known
     const double* __restrict__ e_h = CORRECTOR ? B.Bh : B.Ah;
@@ -220,7 +234,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         const bool own_col = lane >= HALO && lane < HALO + M_OWN && gi < nx;
         const bool fastx = i0 - HALO >= 0 && i0 - HALO + 32 <= nx;   // all 32 columns inside (warp-uniform)
         auto prim = [&](double h, double hu, double hv, double z, MPrim& m) {
-            const double rh = (h > h_eps) ? drcp(h) : 0.0;
+            const double rh = drcp_sel(h > h_eps, h);
             m.h = h;
             m.e = h + z;
             m.u = hu * rh;
@@ -254,10 +268,17 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         long long onx = (long long)(j0 + 1) * pitch + gi;
         long long ofn = (long long)(j0 - 2) * pitch + gi;
         bool dA = DRY && __all_sync(0xffffffffu, A.h == 0.0), dB = DRY && __all_sync(0xffffffffu, Bw.h == 0.0);
-_Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
-        for (int j = j0; j <= jend + 1; ++j) {
+        // this lane's clamp bookkeeping, flushed once after the march: no atomics in the row body
+        unsigned int ncl = 0;
+        double clm = 0.0, clx = 0.0;
+        int clf = 0;                                  // row of this lane's largest clamp
+        // one row j of the march.  FACE: the y face (j-2 | j-1) is formed (j >= j0 + 1); FIN: row j-2 is
+        // finalised (j >= j0 + 2).  The prologue rows j0, j0 + 1 run without them, the steady-state rows with
+        // both, so the steady-state body has no branch but the fetch's warp-uniform ghost test.
+        auto row = [&](const int j, auto face_t, auto fin_t) {
+            constexpr bool FACE = decltype(face_t)::value, FIN = decltype(fin_t)::value;
             prim(rh_, rhu, rhv, rz, C);
-            if (j <= jend) {
+            {   // row j + 1 (the last row's fetch, past jend + 1, is never used: a valid cell or ghost)
                 const int jn = j + 1;
                 if (fastx && jn < ny) {
                     const size_t on = (size_t)onx;
@@ -273,21 +294,23 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
             // the finalised row's own state, issued early; unconditional loads (a non-own lane reads cell
             // (0, 0), always allocated) keep the loop free of divergent branches
             const int f = j - 2;
-            const bool own = own_col && f >= j0;
+            const bool own = FIN && own_col;
             const size_t o = own ? (size_t)ofn : 0;
             onx += pitch;
             ofn += pitch;
             SWOF_ASSERT(!own || (f >= 0 && f < ny && gi >= 0 && gi < nx));
-            double V = 0.0, cf = P.fric_coef, Ah0 = 0.0, Ahu0 = 0.0, Ahv0 = 0.0, VA0 = 0.0;
-            const double hus = in_hu[o];
-            const double hvs = in_hv[o];
-            if (ph_ga<PH>(P)) V = CORRECTOR ? B.VB[o] : B.VA[o];
-            if (ph_ff<PH>(P)) cf = B.fric[o];
-            if (CORRECTOR) {
-                Ah0 = B.Ah[o];
-                Ahu0 = B.Ahu[o];
-                Ahv0 = B.Ahv[o];
-                if (ph_ga<PH>(P)) VA0 = B.VA[o];
+            double V = 0.0, cf = P.fric_coef, Ah0 = 0.0, Ahu0 = 0.0, Ahv0 = 0.0, VA0 = 0.0, hus = 0.0, hvs = 0.0;
+            // issued here, unconditionally (volatile: the compiler may not sink them into the own-lane store
+            // branch, where their DRAM latency would be exposed)
+            if (FIN) hus = ld_early(in_hu + o);
+            if (FIN) hvs = ld_early(in_hv + o);
+            if (FIN && ph_ga<PH>(P)) V = ld_early((CORRECTOR ? B.VB : B.VA) + o);
+            if (FIN && ph_ff<PH>(P)) cf = ld_early(B.fric + o);
+            if (FIN && CORRECTOR) {
+                Ah0 = ld_early(B.Ah + o);
+                Ahu0 = ld_early(B.Ahu + o);
+                Ahv0 = ld_early(B.Ahv + o);
+                if (ph_ga<PH>(P)) VA0 = ld_early(B.VA + o);
             }
             // DRY: warp rows whose 32 cells all hold h = 0 (carried: dA, dB of rows j-2, j-1; dC of row j)
             const bool dC = DRY && __all_sync(0xffffffffu, C.h == 0.0);
@@ -301,14 +324,14 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                 minusB = recon_minus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
                 plusB = recon_plus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
             }
-            if (j - 1 >= j0) {
+            if (FACE) {
                 // y face between rows j-2 and j-1: the north face of row j-2, the south face of row j-1
                 double2 nfa = z2, nfb = z2;
                 if (!(DRY && dA && dB)) {
                     if (M_SLOW(face_flux<false>(P.g, h_eps, plusA, minusB, nfa, nfb, rus)))
                         face_flux<true>(P.g, h_eps, plusA, minusB, nfa, nfb, rus);
                 }
-                if (j - 2 >= j0) {
+                if (FIN) {
                     // ---- finalise row f = j-2 (window A): x direction by shuffles, update, sources ----
                     double2 wa = z2, wb = z2, ea = z2, eb = z2;   // west / east face of this lane's cell
                     double Fcx = 0.0;
@@ -348,38 +371,35 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
                     double hst, hu2, hv2, Vn;
                     if (M_SLOW(cell_sources<PH, false>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn)))
                         cell_sources<PH, true>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn);
-                    if (cl > 0.0) {
-                        atomicAdd(&st->clamps, 1ull);
-                        atomicAdd(&st->clamped_mass, cl);
-                        if (atomicMax(&st->clamp_max_bits, d2u(cl)) < d2u(cl)) {
-                            atomicExch((unsigned long long*)&st->big_clamp_cell, (unsigned long long)((long long)f * nx + gi));
-                            atomicExch((unsigned long long*)&st->big_clamp_step, (unsigned long long)st->step[par]);
+                    ncl += cl > 0.0 ? 1u : 0u;
+                    clm += cl;
+                    clf = cl > clx ? f : clf;
+                    clx = cl > clx ? cl : clx;
+                    // the values this lane stores: U* (predictor) or the Heun average U^{n+1} (corrector), and
+                    // the corrector's CFL speeds, all formed before the own-lane store branch (so the loads of
+                    // U^n stay early and the speeds' rcp / sqrt chains overlap the rest of the row)
+                    double oh = hst, ohu = hu2, ohv = hv2, oV = Vn;
+                    if (CORRECTOR) {
+                        oh = 0.5 * (Ah0 + hst);
+                        ohu = 0.5 * (Ahu0 + hu2);
+                        ohv = 0.5 * (Ahv0 + hv2);
+                        oV = 0.5 * (VA0 + Vn);
+                        if (P.cfl_mode == 0) {
+                            double su, sv;
+                            if (M_SLOW(cfl_speeds<false>(P, oh, ohu, ohv, su, sv))) cfl_speeds<true>(P, oh, ohu, ohv, su, sv);
+                            amx = (own && (su > amx || su != su)) ? su : amx;
+                            amy = (own && (sv > amy || sv != sv)) ? sv : amy;
                         }
-                        if (cl > P.clamp_fail) atomicOr(&st->flags, FLAG_BIGCLAMP);
                     }
                     if (own) {
-                        if (!CORRECTOR) {
-                            B.Bh[o] = hst;
-                            B.Bhu[o] = hu2;
-                            B.Bhv[o] = hv2;
-                            if (ph_ga<PH>(P)) B.VB[o] = Vn;
-                            if (PUSH && (f < GHOST_ROWS || f >= ny - GHOST_ROWS)) push_halo(B, 1, ny, pitch, f, gi, hst, hu2, hv2);
-                        } else {
-                            const double hN = 0.5 * (Ah0 + hst);
-                            const double huN = 0.5 * (Ahu0 + hu2);
-                            const double hvN = 0.5 * (Ahv0 + hv2);
-                            B.Ah[o] = hN;
-                            B.Ahu[o] = huN;
-                            B.Ahv[o] = hvN;
-                            if (ph_ga<PH>(P)) B.VA[o] = 0.5 * (VA0 + Vn);
-                            if (PUSH && (f < GHOST_ROWS || f >= ny - GHOST_ROWS)) push_halo(B, 0, ny, pitch, f, gi, hN, huN, hvN);
-                            if (P.cfl_mode == 0) {   // own lanes only (divergent: no warp vote here)
-                                double su, sv;
-                                if (cfl_speeds<false>(P, hN, huN, hvN, su, sv)) cfl_speeds<true>(P, hN, huN, hvN, su, sv);
-                                amx = (su > amx || su != su) ? su : amx;
-                                amy = (sv > amy || sv != sv) ? sv : amy;
-                            }
-                        }
+                        double* const oA = CORRECTOR ? B.Ah : B.Bh;
+                        double* const oAu = CORRECTOR ? B.Ahu : B.Bhu;
+                        double* const oAv = CORRECTOR ? B.Ahv : B.Bhv;
+                        oA[o] = oh;
+                        oAu[o] = ohu;
+                        oAv[o] = ohv;
+                        if (ph_ga<PH>(P)) (CORRECTOR ? B.VA : B.VB)[o] = oV;
+                        if (PUSH && (f < GHOST_ROWS || f >= ny - GHOST_ROWS)) push_halo(B, CORRECTOR ? 0 : 1, ny, pitch, f, gi, oh, ohu, ohv);
                     }
                 }
                 sfa = make_double2(nfa.x, nfa.y);              // becomes the south face of row j-1
@@ -392,6 +412,19 @@ _Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
             slA = saB;
             A = Bw;
             Bw = C;
+        };
+        row(j0, std::false_type{}, std::false_type{});
+        row(j0 + 1, std::true_type{}, std::false_type{});
+_Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
+        for (int j = j0 + 2; j <= jend + 1; ++j) row(j, std::true_type{}, std::true_type{});
+        if (__any_sync(0xffffffffu, ncl != 0u) && ncl != 0u) {   // rare: a clamp in this warp's segment
+            atomicAdd(&st->clamps, (unsigned long long)ncl);
+            atomicAdd(&st->clamped_mass, clm);
+            if (atomicMax(&st->clamp_max_bits, d2u(clx)) < d2u(clx)) {
+                atomicExch((unsigned long long*)&st->big_clamp_cell, (unsigned long long)((long long)clf * nx + gi));
+                atomicExch((unsigned long long*)&st->big_clamp_step, (unsigned long long)st->step[par]);
+            }
+            if (clx > P.clamp_fail) atomicOr(&st->flags, FLAG_BIGCLAMP);
         }
     }
     if (CORRECTOR) {

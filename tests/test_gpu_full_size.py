@@ -6,8 +6,9 @@ sequence and of the packed wet mask) and tests/golden/full_size/<cfg>.npz (the w
 final state at 4096 seeded sample cells).
 
 North_star tolerances: max |dh|, |dhu|, |dhv| (and |dV|) <= 1e-8 after the full count -- checked on the
-samples, and on every cell when the digests agree (equal digests = equal rasters bit for bit) --, the wet/dry
-mask identical (its digest), the dt sequence equal to 1e-13 relative, the same step count and final time.
+samples --, the wet/dry mask identical (its digest), the dt sequence equal to 1e-13 relative, the same step
+count and final time; and, the kernels being bit-identical to the oracle (DESIGN.md §3 "contract"), equal
+digests: every cell of every field and every dt equal bit for bit.
 A configuration whose digest was not generated yet is skipped with that reason; a digest whose oracle or
 workload sources changed since it was written fails (it would no longer describe this oracle).
 """
@@ -79,3 +80,4 @@ def test_full_size_full_count(gpu, name):
     bitwise = (_sha(g["h"]) == ent["sha_h"] and _sha(g["hu"]) == ent["sha_hu"] and _sha(g["hv"]) == ent["sha_hv"]
                and (cfg.ga is None or _sha(g["v"]) == ent["sha_v"]) and _sha(dt) == ent["sha_dt"])
     print(name, g["step"], "steps, sampled worst", worst, "bitwise (every cell, digests)", bitwise)
+    assert bitwise
