@@ -5,11 +5,13 @@ BASELINE.json throughput/roofline configuration), fp64, 1 x B200 per rank.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg4]
     python bench.py --workload d8 [--steps K] [--warmup W] [--d8-dtype f32|f64]
 
-N > 1 is launched by torchrun; every rank advances its own full cfg4 replica (the north star excludes
-domain decomposition: "replicas only", weak scaling, no data-path collective).  Timing: W untimed
-steps, then exactly K steps bracketed by barrier + cuda synchronize, CUDA events on the context's
-stream, max over ranks.  The inputs (4.6 GB of fields) are far larger than the 126 MB L2, so no flush
-is needed between steps.  Rank 0 prints one JSON line.
+N > 1 is launched by torchrun; the ONE cfg4 grid is cut into row strips, one per rank (the paper's MPI
+decomposition P:731-760; strong scaling): per step two NCCL halo exchanges of 2 rows x 3 fields
+with each neighbour and one all-reduce(max) of the 2 CFL words (--shard-fused: the kernels push the boundary
+rows into the neighbours' CUDA-IPC-mapped ghost rows instead).  --replicas runs N independent full replicas
+(weak scaling, no data-path collective) instead.  Timing: W untimed steps, then exactly K steps bracketed by
+barrier + cuda synchronize, CUDA events on the context's stream, max over ranks.  The inputs (4.6 GB of
+fields) are far larger than the 126 MB L2, so no flush is needed between steps.  Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -145,10 +147,18 @@ def cpu_sample(cfg, crop: int, steps: int):
         setattr(sub, k, None if a is None else np.ascontiguousarray(a[sl]))
     sub.bc = {"W": "wall", "E": "wall", "S": "wall", "N": "wall"}
     sub.inflow = {}
-    t0 = time.perf_counter()
-    r = oracle.run(sub, nsteps=steps, t_end=float("inf"))
-    secs = time.perf_counter() - t0
-    return crop * crop * r["steps"] / secs, r["counters"], secs, r["steps"]
+    host = host_info()
+    old = os.sched_getaffinity(0)
+    core = max(old)                                   # pin the single-threaded oracle to one core
+    os.sched_setaffinity(0, {core})
+    try:
+        t0 = time.perf_counter()
+        r = oracle.run(sub, nsteps=steps, t_end=float("inf"))
+        secs = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, old)
+    host["pinned_core"] = core
+    return crop * crop * r["steps"] / secs, r["counters"], secs, r["steps"], host
 
 
 def f_alg_from_counters(cnt, cfg, steps, cells):
@@ -164,6 +174,84 @@ def f_alg_from_counters(cnt, cfg, steps, cells):
             ops += cnt.cell_wet_fric * OPS_FIELD
     ops += steps * cells * OPS_STEP
     return ops / (steps * cells)
+
+def host_info():
+    """CPU model, nproc and the core the oracle sample is pinned to (SURVEY.md §8d timing protocol)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def fp64_issue_ceiling(peak_gops):
+    """The FP64-pipe ceiling of the kernels' own instruction mix: the pipe's lane-op rate over the executed fp64
+    lane-instructions per cell-update (DMUL/DADD/DFMA/DSETP warp-instructions per cell x 32, predictor +
+    corrector) from the committed ncu capture (profiles/ncu_latest.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
+            prof = json.load(f)
+        per_cell = 0.0
+        for k in prof["kernels"].values():
+            mix = k.get("opcode_mix_per_cell", {})
+            per_cell += sum(mix.get(op, 0.0) for op in ("DMUL", "DADD", "DFMA", "DSETP", "DMNMX"))
+        if per_cell <= 0:
+            return None
+        return {"value": peak_gops * 1e9 / (32 * per_cell), "unit": UNIT,
+                "fp64_lane_instr_per_cell_update": 32 * per_cell,
+                "source": f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"}
+    except Exception:
+        return None
+
+
+def roofline(peaks, src, peak_gops, f_alg, dom, dom_ms, dom_bytes, cells, value, ga, field):
+    """SURVEY.md §8d.  The dominant kernel against both of its floors -- HBM (algorithmic bytes / launch time
+    vs the measured copy bandwidth) and the fp64 pipe (algorithmic ops, div/sqrt/cube root = 1, vs 148 x 64
+    lanes x clock) -- `bound` being the one with the larger fraction; and the whole step against R_2k (the
+    per-stage design's bytes) and R_alg (the step-fused minimum bytes; the headline of §8d)."""
+    hbm = peaks["hbm_gbs"]
+    hbm_ach = dom_bytes / (dom_ms / 1e3) / 1e9
+    # dominant kernel's algorithmic fp64 ops: the per-stage half of the per-cell work, plus (corrector) the
+    # per-step Heun + CFL ops
+    ops_dom = (f_alg - OPS_STEP) / 2 + (OPS_STEP if dom == "corrector" else 0)
+    fp_ach = ops_dom * cells / (dom_ms / 1e3) / 1e9
+    frac_h, frac_f = hbm_ach / hbm, fp_ach / peak_gops
+    traffic, tsrc, ncu = None, None, None
+    try:   # DRAM read+write per launch of the same kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
+            prof = json.load(f)
+        for kname, k in prof["kernels"].items():
+            is_corr = re.search(r"(stage|march)_kernel<(\(bool\))?(1|true)\b", kname) is not None
+            if is_corr == (dom == "corrector"):
+                traffic = k["dram_bytes_per_cell"] * cells
+                tsrc = f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"
+                ncu = {"fp64_pipe_pct": k.get("fp64_pipe_pct"), "issue_active_pct": k.get("issue_active_pct"),
+                       "dram_throughput_pct": k.get("dram_throughput_pct"), "registers": k.get("registers"),
+                       "warps_active_pct": k.get("warps_active_pct")}
+    except Exception:
+        pass
+    b2k = sum(bytes_per_cell_update(ga, field))
+    balg = 8 * (4 + ga + field) + 8 * (3 + ga)              # read U^n, z (+V, +n); write U^{n+1} (+V)
+    r_fp = peak_gops * 1e9 / f_alg
+    r_2k = min(hbm * 1e9 / b2k, r_fp)
+    r_alg = min(hbm * 1e9 / balg, r_fp)
+    hb = {"achieved": hbm_ach, "peak": hbm, "unit": "GB/s", "frac": frac_h, "peak_source": src}
+    fb = {"achieved": fp_ach, "peak": peak_gops, "unit": "Gop/s (fp64 lane-ops)", "frac": frac_f,
+          "ops_per_cell": ops_dom, "peak_note": f"148 SMs x 64 fp64 lanes x {peaks.get('sm_max_mhz', 1965.0):.0f} MHz"}
+    b = hb if frac_h >= frac_f else fb
+    return {"bound": "hbm" if frac_h >= frac_f else "alu", "achieved": b["achieved"], "peak": b["peak"],
+            "unit": b["unit"], "frac": b["frac"], "traffic": traffic, "traffic_unit": "bytes/launch",
+            "traffic_source": tsrc, "kernel": dom, "algorithmic_bytes": dom_bytes,
+            "floors": {"hbm": hb, "fp64": fb}, "ncu": ncu,
+            "step": {"R_2k": r_2k, "R_alg": r_alg, "B_2k": b2k, "B_alg": balg, "F_alg": f_alg,
+                     "frac_R_2k": value / r_2k, "frac_R_alg": value / r_alg,
+                     "R_2k_bound": "hbm" if hbm * 1e9 / b2k <= r_fp else "fp64",
+                     "R_alg_bound": "hbm" if hbm * 1e9 / balg <= r_fp else "fp64"},
+            "fp64_issue_ceiling": fp64_issue_ceiling(peak_gops)}
 
 
 def main():
@@ -183,8 +271,10 @@ def main():
                     help="with --shard: fused exchange (kernels push boundary rows into the neighbours' "
                          "CUDA-IPC-mapped ghost rows) and in-stream NCCL barriers")
     ap.add_argument("--shard", action="store_true",
-                    help="N > 1: split the one grid into row strips over the ranks (strong scaling, NCCL halo "
-                         "exchange + CFL all-reduce per step) instead of N independent replicas")
+                    help="split the one grid into row strips over the ranks (strong scaling, NCCL halo exchange + "
+                         "CFL all-reduce per step); the default for N > 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent full replicas (weak scaling) instead of the row-strip decomposition")
     ap.add_argument("--d8-dtype", default="f32", choices=("f32", "f64"))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -195,7 +285,7 @@ def main():
         return reference_arm(args, rank, world)
     if args.workload == "d8":
         return bench_d8(args, rank, world, local)
-    if args.shard:
+    if args.shard or args.shard_fused or (world > 1 and not args.replicas):
         return bench_shard(args, rank, world, local)
 
     import torch
@@ -295,40 +385,17 @@ def main():
     }
 
     fmax_mhz = peaks.get("sm_max_mhz", 1965.0)
-    peak_gops = 148 * 64 * fmax_mhz * 1e6 / 1e9        # fp64 lanes x SMs x clock
+    peak_gops = 148 * 64 * fmax_mhz * 1e6 / 1e9        # fp64 lane-ops/s: SMs x fp64 lanes x clock
     f_alg = None
     if not args.no_cpu_baseline:
-        rate, cnt, secs, nst = cpu_sample(cfg, min(args.cpu_crop, cfg.nx, cfg.ny), args.cpu_steps)
         crop = min(args.cpu_crop, cfg.nx, cfg.ny)
+        rate, cnt, secs, nst, host = cpu_sample(cfg, crop, args.cpu_steps)
         f_alg = f_alg_from_counters(cnt, cfg, nst, crop * crop)
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                                "sample": f"{crop}x{crop} centre crop of {args.config}, {nst} Heun steps, "
-                                         f"walls, {secs:.1f} s single-threaded"}
+                                         f"walls, {secs:.1f} s single-threaded", **host}
     if f_alg is not None:
-        # dominant kernel's algorithmic fp64 ops: about half the per-step ops each (per-stage work)
-        frac_dom = (OPS_STEP / 2 + (f_alg - OPS_STEP) / 2) / f_alg if dom == "predictor" else \
-            ((f_alg - OPS_STEP) / 2 + OPS_STEP) / f_alg
-        ach = f_alg * frac_dom * cells / (dom_ms / 1e3) / 1e9
-        traffic, tsrc = None, None
-        try:   # DRAM read+write per launch of the same kernel from the committed ncu --set full capture
-            with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
-                prof = json.load(f)
-            for kname, k in prof["kernels"].items():
-                is_corr = re.search(r"(stage|march)_kernel<(\(bool\))?(1|true)\b", kname) is not None
-                if is_corr == (dom == "corrector"):
-                    traffic = k["dram_bytes_per_cell"] * cells
-                    tsrc = f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"
-                    out["ncu_dominant_kernel"] = {  # context from the same capture: what bounds the kernel
-                        "fp64_pipe_pct": k.get("fp64_pipe_pct"), "issue_active_pct": k.get("issue_active_pct"),
-                        "dram_throughput_pct": k.get("dram_throughput_pct"), "registers": k.get("registers"),
-                        "warps_active_pct": k.get("warps_active_pct")}
-        except Exception:
-            pass
-        out["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak_gops, "unit": "Gop/s (fp64)",
-                           "frac": ach / peak_gops, "traffic": traffic, "traffic_unit": "bytes/launch",
-                           "traffic_source": tsrc, "algorithmic_bytes": dom_bytes, "kernel": dom,
-                           "f_alg_per_cell_update": f_alg,
-                           "peak_note": f"148 SMs x 64 fp64 lanes x {fmax_mhz:.0f} MHz (sm_max, {src})"}
+        out["roofline"] = roofline(peaks, src, peak_gops, f_alg, dom, dom_ms, dom_bytes, cells, value, ga, field)
     print(json.dumps(out), flush=True)
     solver.close()
     if world > 1:
@@ -370,9 +437,26 @@ def bench_shard(args, rank, world, local):
     if world > 1:
         dist.barrier()
     ms = reduce_max(e0.elapsed_time(e1), world, "cuda")
+    # end to end: the host state in (every rank loads its strip), K steps, the state out
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    s.set_state(cfg.h, cfg.hu, cfg.hv, cfg.vinf if cfg.ga is not None else None, 0.0)
+    s.step(args.steps)
     st = s.get_state()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = reduce_max(e2.elapsed_time(e3), world, "cuda")
     s.close()
     if rank == 0:
+        peaks, src = load_peaks()
+        ga, field = cfg.ga is not None, cfg.fric_field is not None
+        b2k = sum(bytes_per_cell_update(ga, field))
+        ach = b2k * (cells / world) * args.steps / (ms / 1e3) / 1e9      # per rank (strip), whole step
+        nfield = 3 + ga
+        io = nfield * cells * 8
         out = {"metric": METRIC, "value": cells * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -383,6 +467,14 @@ def bench_shard(args, rank, world, local):
                                                                      "NCCL halo exchange") + " + CFL all-reduce)",
                           "l2": "inputs larger than L2; no flush"},
                "gpu_launches": args.steps * (2 + (cfg.cfl_mode == "face")), "clocks": clk.summary(),
+               "e2e": {"value": cells * args.steps / (ms_e2e / 1e3), "unit": UNIT,
+                       "h2d_bytes_per_step": io / args.steps, "d2h_bytes_per_step": io / args.steps,
+                       "note": "set_state of the host state into every strip + K steps + get_state"},
+               "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                            "frac": ach / peaks["hbm_gbs"], "traffic": None, "kernel": "whole step per strip",
+                            "algorithmic_bytes_per_cell_update": b2k, "peak_source": src,
+                            "note": "multi-GPU line: the step time includes the halo exchange; per-kernel "
+                                    "fractions are on the N=1 line"},
                "t": st["t"], "step": st["step"]}
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -461,10 +553,11 @@ def bench_d8(args, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak",
             # the paper's one D8 pass over a 14786 x 10086 DEM took 31 s with SkelGIS (101 s
-            # with SkeTo) on unspecified CPU hardware -- context, another machine
-            "vs_baseline": value / (npts / 31.0),
-            "baseline": {"paper_seconds_per_pass": 31.0, "system": "SkelGIS, unspecified CPU hardware",
-                         "source": "BASELINE.md / PAPER.md:604-612"},
+            # with SkeTo) on unspecified CPU hardware: a comparison system on another
+            # machine -- context only, not a baseline
+            "vs_baseline": None,
+            "context": {"paper_seconds_per_pass": 31.0, "system": "SkelGIS (SkeTo 101 s), unspecified CPU hardware",
+                        "source": "BASELINE.md / PAPER.md:604-612", "ratio_to_paper_pass": value / (npts / 31.0)},
             "dtype": args.d8_dtype,
             "data": "synthetic (seeded sinusoid DEM, 1 cm quantised, no-data disc; workloads/dem.py)",
             "config": {"workload": "d8 dem_large", "nx": nx, "ny": ny, "points": npts,
@@ -521,15 +614,15 @@ def reference_arm(args, rank, world):
     cfg = make(args.config, nx=args.nx, ny=args.ny)
     crop = min(512, cfg.nx, cfg.ny)
     # warm-up then timed steps, each a single Heun step of the crop
-    rate_w, _, _, _ = cpu_sample(cfg, crop, args.warmup)
-    rate, cnt, secs, nst = cpu_sample(cfg, crop, args.steps)
+    cpu_sample(cfg, crop, args.warmup)
+    rate, cnt, secs, nst, host = cpu_sample(cfg, crop, args.steps)
     out = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": secs * 1e3 / max(nst, 1), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": args.config, "nx": cfg.nx, "ny": cfg.ny, "sample": f"{crop}x{crop} crop"},
            "impl": "reference",
            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": f"{crop}x{crop} centre crop of {args.config}, {nst} Heun steps"},
+                            "sample": f"{crop}x{crop} centre crop of {args.config}, {nst} Heun steps", **host},
            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "gpu_launches": 0}
     print(json.dumps(out), flush=True)

@@ -22,6 +22,7 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["steps"] == 2 and d["warmup"] == 3 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
+    assert d["cpu_baseline"]["nproc"] >= 1 and "pinned_core" in d["cpu_baseline"]
     assert d["config"]["workload"] == "cfg0" and d["dtype"] == "f64"
 
 

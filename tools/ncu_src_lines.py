@@ -51,7 +51,7 @@ for l in dis.split("\n"):
         pairs = re.findall(r'"([^"]+)", line (\d+)', l)
         pairs = [(Path(f).name, int(n)) for f, n in pairs]
         outer = [p for p in pairs if p[0] == kfile]
-        cur = (outer[-1] if outer else None, pairs[0] if pairs else None)
+        cur = (outer[-1] if outer else None, pairs[0] if pairs else None, outer[0] if outer else None)
         continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", l)
     if m:
@@ -60,6 +60,7 @@ sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-s
                       text=True).stdout
 per_outer = collections.defaultdict(lambda: [0, 0])
 per_inner = collections.defaultdict(lambda: [0, 0])
+per_kin = collections.defaultdict(lambda: [0, 0])
 kern, take, base = None, False, None
 seen = set()
 for r in csv.reader(io.StringIO(sass)):
@@ -76,7 +77,7 @@ for r in csv.reader(io.StringIO(sass)):
     if take and len(r) > 5:
         a = int(r[0], 16)
         base = a if base is None else base
-        o, i = info.get(a - base, (None, None))
+        o, i, k_in = info.get(a - base, (None, None, None))
         smp = int(r[h.index("Warp Stall Sampling (All Samples)")] or 0)
         ins = int(r[h.index("Instructions Executed")] or 0)
         if opfilter:
@@ -88,7 +89,10 @@ for r in csv.reader(io.StringIO(sass)):
         per_outer[o][1] += ins
         per_inner[i][0] += smp
         per_inner[i][1] += ins
-for title, d in (("call site (" + kfile + ")", per_outer), ("innermost line", per_inner)):
+        per_kin[k_in][0] += smp
+        per_kin[k_in][1] += ins
+for title, d in (("call site (" + kfile + ")", per_outer), ("innermost line in " + kfile, per_kin),
+                 ("innermost line", per_inner)):
     ts = sum(v[0] for v in d.values()) or 1
     ti = sum(v[1] for v in d.values()) or 1
     print(f"== by {title}: {ti} warp-instructions")
