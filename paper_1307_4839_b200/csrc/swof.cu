@@ -17,6 +17,10 @@
 #include "swof_kernels.cuh"
 #include "swof_d8.cuh"
 #include "swof_march.cuh"
+#if SWOF_MARCH_TMA
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#endif
 
 using namespace swof;
 
@@ -39,6 +43,7 @@ struct swof_ctx {
     dim3 cf_grid;                               // face-CFL pass tiles
     dim3 sgrid, sblock;                         // stage kernel launch shape
     size_t ssmem = 0;
+    void* d_tmaps = nullptr;                    // SWOF_MARCH_TMA builds: the 8 tensor maps (KBufs::tmaps)
     std::string err;
 };
 
@@ -324,6 +329,34 @@ static int choose_kernels(swof_ctx* c) {
     }
 }
 
+#if SWOF_MARCH_TMA
+// the TMA tensor maps of the marching kernel's row ring (swof_march.cuh): for the predictor's input A and the
+// corrector's input B, {h, hu, hv, z} as 2-D f64 tensors of nx x (ny + 2 GHOST_ROWS) elements (the spare rows
+// included), row stride = the pitch, box 32 x TMA_ROWS; built once per context
+static int make_tmaps(swof_ctx* c, const Layout& L) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return 1;
+    auto encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    CUtensorMap maps[8];
+    const KBufs& b = c->kb;
+    double* f[8] = {b.Ah, b.Ahu, b.Ahv, b.z, b.Bh, b.Bhu, b.Bhv, b.z};
+    for (int k = 0; k < 8; ++k) {
+        const cuuint64_t dims[2] = {(cuuint64_t)c->p.nx, (cuuint64_t)c->p.ny + 2 * GHOST_ROWS};
+        const cuuint64_t strides[1] = {(cuuint64_t)L.pitch * sizeof(double)};
+        const cuuint32_t box[2] = {32, (cuuint32_t)TMA_ROWS};
+        const cuuint32_t es[2] = {1, 1};
+        if (encode(&maps[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, f[k] - (size_t)GHOST_ROWS * L.pitch, dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) return 1;
+    }
+    if (cudaMalloc(&c->d_tmaps, sizeof(maps)) != cudaSuccess) return 1;
+    if (cudaMemcpy(c->d_tmaps, maps, sizeof(maps), cudaMemcpyHostToDevice) != cudaSuccess) return 1;
+    c->kb.tmaps = c->d_tmaps;
+    return 0;
+}
+#endif
+
 int swof_create(const swof_params* p, const double* z, const double* fric_field, void* d_workspace, size_t ws_bytes,
                 void* cuda_stream, swof_ctx** out) {
     if (!out) return SWOF_EINVAL;
@@ -361,6 +394,7 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
     b.st = (DevState*)(base + L.off_st);
     std::memset(b.push, 0, sizeof(b.push));
     b.push_any = 0;
+    b.tmaps = nullptr;
     b.dt_hist = (double*)(base + L.off_hist);
     b.dt_cap = p->dt_hist_cap > 0 ? p->dt_hist_cap : (int64_t)1 << 20;
     c->d_part = (double*)(base + L.off_part);
@@ -411,6 +445,9 @@ int swof_create(const swof_params* p, const double* z, const double* fric_field,
             for (double v : tmp) if (!(v > 0) || !std::isfinite(v)) { swof_destroy(c); return SWOF_EINVAL; }
         }
     }
+#if SWOF_MARCH_TMA
+    if (make_tmaps(c, L)) { swof_destroy(c); return SWOF_ECUDA; }
+#endif
     *out = c;
     return SWOF_OK;
 }
@@ -800,6 +837,7 @@ void swof_destroy(swof_ctx* c) {
     if (c->graph) cudaGraphExecDestroy(c->graph);
     if (c->own_ws && c->ws) cudaFree(c->ws);
     if (c->h_st) cudaFreeHost(c->h_st);
+    if (c->d_tmaps) cudaFree(c->d_tmaps);
     delete c;
 }
 

@@ -47,6 +47,28 @@ constexpr int M_NW = SWOF_MARCH_NW;    // warps per CTA (independent); rows per 
 
 struct MPrim { double h, e, u, v, rh; };
 
+// ---- SWOF_MARCH_TMA (experiment, DESIGN.md §5 "TMA"): the next row of an interior warp comes from a
+// shared-memory ring fed by TMA tensor-map loads (cp.async.bulk.tensor, UTMALDG) instead of 4 LDG per lane
+#ifndef SWOF_MARCH_TMA
+#define SWOF_MARCH_TMA 0
+#endif
+constexpr int TMA_ROWS = 4;            // rows per TMA box (32 columns x 4 rows x 8 B = 1 KB per field)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 :: "r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar)) : "memory");
+}
+
 // a global load issued at its program point (volatile asm is neither removed nor moved past other volatile
 // asm; the value is still scheduled like any register)
 __device__ __forceinline__ double ld_early(const double* p) {
@@ -233,6 +255,35 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         const int gi = i0 - HALO + lane;
         const bool own_col = lane >= HALO && lane < HALO + M_OWN && gi < nx;
         const bool fastx = i0 - HALO >= 0 && i0 - HALO + 32 <= nx;   // all 32 columns inside (warp-uniform)
+#if SWOF_MARCH_TMA
+        // TMA ring: rows j0+1 .. jend+2 (the fetched rows) in chunks of TMA_ROWS, two stages; only for warps whose
+        // fetched rows are all stored rows (interior strips, not the last segment: its ghosts are synthesised)
+        __shared__ alignas(128) double s_ring[2][4][TMA_ROWS][32];
+        __shared__ alignas(8) unsigned long long s_bar[2];
+        const bool tma = B.tmaps != nullptr && fastx && jend + 1 < ny && j0 >= 2;
+        const int nchunk = (jend - j0 + 2 + TMA_ROWS - 1) / TMA_ROWS;
+        const char* tm = (const char*)B.tmaps + (CORRECTOR ? 4 * 128 : 0);
+        auto tma_issue = [&](int c) {          // lane 0: chunk c into stage c & 1
+            if (lane == 0 && c < nchunk) {
+                unsigned long long* bar = &s_bar[c & 1];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(bar, 4u * TMA_ROWS * 32 * 8);
+                const int y = j0 + 1 + c * TMA_ROWS + GHOST_ROWS;          // tensor rows start at field row -2
+#pragma unroll
+                for (int f = 0; f < 4; ++f) tma_load_2d(&s_ring[c & 1][f][0][0], tm + f * 128, i0 - HALO, y, bar);
+            }
+        };
+        if (tma) {
+            if (lane == 0) {
+                mbar_init(&s_bar[0], 1);
+                mbar_init(&s_bar[1], 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            __syncwarp();
+            tma_issue(0);
+            tma_issue(1);
+        }
+#endif
         auto prim = [&](double h, double hu, double hv, double z, MPrim& m) {
             const double rh = drcp_sel(h > h_eps, h);
             m.h = h;
@@ -280,6 +331,21 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
             prim(rh_, rhu, rhv, rz, C);
             {   // row j + 1 (the last row's fetch, past jend + 1, is never used: a valid cell or ghost)
                 const int jn = j + 1;
+#if SWOF_MARCH_TMA
+                if (tma) {
+                    const int k = jn - (j0 + 1), c = k / TMA_ROWS, r = k - c * TMA_ROWS;
+                    if (r == 0) {
+                        // chunk c - 1 (stage (c + 1) & 1) was read by the previous rows and its values are used:
+                        // refill that stage with chunk c + 1, then wait for chunk c
+                        if (c >= 1) tma_issue(c + 1);
+                        mbar_wait(&s_bar[c & 1], (c >> 1) & 1);
+                    }
+                    rh_ = s_ring[c & 1][0][r][lane];
+                    rhu = s_ring[c & 1][1][r][lane];
+                    rhv = s_ring[c & 1][2][r][lane];
+                    rz = s_ring[c & 1][3][r][lane];
+                } else
+#endif
                 if (fastx && jn < ny) {
                     const size_t on = (size_t)onx;
                     SWOF_ASSERT(jn >= 0 && jn < ny && gi >= 0 && gi < nx);
