@@ -1,7 +1,7 @@
 """Build libswof.so (the C-ABI library, include/swof.h) in-tree for sm_100a with nvcc.
 
 libswof.so is the bit-identical build (-DSWOF_EXACT=1 -fmad=false): no multiply-add contraction, the
-evaluation order of every expression is the oracle's canonical sheet, division and sqrt IEEE
+evaluation order of every expression is the canonical sheet of DESIGN.md §3, division and sqrt IEEE
 (nvcc defaults: -prec-div=true -prec-sqrt=true -ftz=false).  tolerance=True builds the measured-and-rejected
 tolerance-contract variant (-DSWOF_EXACT=0 -fmad=true; DESIGN.md §3 "contract") into another file, for
 A/B experiments only.

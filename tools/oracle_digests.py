@@ -12,6 +12,12 @@ the same inputs and compares digests: equal digests mean the GPU state equals th
 (hence within every north_star tolerance, masks and dt sequence included).
 
     OMP_NUM_THREADS=7 python tools/oracle_digests.py cfg1 cfg2 cfg4 cfg3
+    python tools/oracle_digests.py cfg3 --ckpt /tmp/swof_ckpt --max-seconds 3000   # resumable, in chunks
+
+With --ckpt the run advances in chunks of 50 steps and, when --max-seconds is spent, saves the state (h, hu, hv,
+V, t), the dt sequence so far and the clamp counters to DIR/<cfg>.npz and exits with status 3; the next call
+resumes from it.  Chunked and unchunked runs give the same state bit for bit (each step is a function of the
+state only; the chunk boundary passes the state through unchanged).
 
 Run time on 8 host cores: cfg1 ~7 min, cfg2 ~15 min, cfg4 ~4 h, cfg3 ~5 h (cfg4 needs ~36 GB of RAM).
 """
@@ -60,7 +66,46 @@ def source_digest() -> str:
     return h.hexdigest()
 
 
-def main(names):
+class _Cnt:
+    def __init__(self, clamps, clamp_max):
+        self.clamps, self.clamp_max = clamps, clamp_max
+
+
+def run_chunked(cfg, name, ckpt, max_seconds, t0, chunk=50):
+    """Advance cfg's full horizon in chunks of `chunk` steps from DIR/<name>.npz (if present); returns
+    (result dict, elapsed oracle seconds incl. earlier calls) when done, or (None, _) after checkpointing."""
+    path = Path(ckpt) / f"{name}.npz"
+    total = cfg.steps if cfg.steps is not None else 1 << 40
+    t_end = cfg.t_end if cfg.t_end is not None else float("inf")
+    if path.exists():
+        c = np.load(path)
+        h, hu, hv = c["h"], c["hu"], c["hv"]
+        v = c["v"] if c["v"].size else None
+        t, dts, clamps, cmax, spent = float(c["t"]), list(c["dt"]), int(c["clamps"]), float(c["cmax"]), float(c["spent"])
+    else:
+        h, hu, hv = cfg.h, cfg.hu, cfg.hv
+        v = cfg.vinf if cfg.ga is not None else None
+        t, dts, clamps, cmax, spent = 0.0, [], 0, 0.0, 0.0
+    while len(dts) < total and t < t_end:
+        r = oracle.run(cfg, h=h, hu=hu, hv=hv, v=v, t0=t, nsteps=min(chunk, total - len(dts)), omp=True)
+        assert r["rc"] == 0, r["rc"]
+        h, hu, hv, v, t = r["h"], r["hu"], r["hv"], r["v"], r["t"]
+        dts.extend(r["dt"].tolist())
+        clamps += int(r["counters"].clamps)
+        cmax = max(cmax, float(r["counters"].clamp_max))
+        if r["steps"] == 0:
+            break
+        if time.time() - t0 > max_seconds and len(dts) < total and t < t_end:
+            Path(ckpt).mkdir(parents=True, exist_ok=True)
+            np.savez(path, h=h, hu=hu, hv=hv, v=(v if v is not None else np.zeros(0)), t=t, dt=np.array(dts),
+                     clamps=clamps, cmax=cmax, spent=spent + time.time() - t0)
+            return None, None
+    res = {"rc": 0, "h": h, "hu": hu, "hv": hv, "v": v, "t": t, "steps": len(dts), "dt": np.array(dts),
+           "counters": _Cnt(clamps, cmax)}
+    return res, spent + time.time() - t0
+
+
+def main(names, ckpt=None, max_seconds=float("inf")):
     data = json.loads(OUT.read_text()) if OUT.exists() else {}
     data["_source"] = ("tools/oracle_digests.py: oracle (OpenMP-over-rows build, bitwise = serial) at each "
                        "configuration's full size and full step count; SHA-256 of the float64 rasters")
@@ -68,9 +113,15 @@ def main(names):
     for name in names:
         cfg = make(name)
         t0 = time.time()
-        r = oracle.run(cfg, omp=True)
-        el = time.time() - t0
-        assert r["rc"] == 0, r["rc"]
+        if ckpt is None:
+            r = oracle.run(cfg, omp=True)
+            el = time.time() - t0
+            assert r["rc"] == 0, r["rc"]
+        else:
+            r, el = run_chunked(cfg, name, ckpt, max_seconds, t0)
+            if r is None:
+                print(name, "checkpointed", flush=True)
+                sys.exit(3)
         h = r["h"]
         ent = {
             "nx": cfg.nx, "ny": cfg.ny, "steps": int(r["steps"]), "t": r["t"], "t_end": cfg.t_end,
@@ -94,4 +145,10 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["cfg1", "cfg2", "cfg4", "cfg3"])
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("names", nargs="*", default=["cfg1", "cfg2", "cfg4", "cfg3"])
+    ap.add_argument("--ckpt", default=None)
+    ap.add_argument("--max-seconds", type=float, default=float("inf"))
+    a = ap.parse_args()
+    main(a.names, a.ckpt, a.max_seconds)
