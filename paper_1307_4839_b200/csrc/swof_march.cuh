@@ -3,39 +3,26 @@
 // columns i0-2 .. i0+29) and marches down a segment of rows (KParams::march_h, chosen at create time).  The
 // y direction (slopes, reconstruction, faces) lives in a 3-row register window, the x direction goes
 // through warp shuffles (neighbour primitives, the left cell's high face, the east face's flux), so there
-// is no shared-memory tile and no barrier in the stencil.  Same arithmetic as the oracle and as the tiled
-// stage_kernel (the canonical sheet of DESIGN.md §3), hence the same bits.  Default (SWOF_MARCH=1); the
-// tiled stage_kernel of swof_kernels.cuh runs in SWOF_MARCH=0 builds.  DESIGN.md §5 has the design and
-// its measurements, §8 the rejected variants (their switches below stay off).
+// is no shared-memory tile and no barrier in the stencil.  Same arithmetic as the oracle (the canonical
+// sheet of DESIGN.md §3), hence the same bits.  DESIGN.md §5 has the design and its measurements, §8 the
+// rejected variants; SWOF_MARCH_TMA=1 builds the TMA-fed experiment (§5 "TMA").
 #pragma once
 #include <type_traits>
 
 namespace swof {
 
 constexpr int M_OWN = 28;              // own columns per warp
-#ifndef SWOF_MARCH_UNROLL
-#define SWOF_MARCH_UNROLL 1
-#endif
-// the rare exact recomputation (SLOW) of an out-of-range lane: per lane (divergent), or, with
-// SWOF_MARCH_VOTE, by the whole warp when any lane needs it (a uniform branch; SLOW gives the same bits)
-#ifndef SWOF_MARCH_VOTE
-#define SWOF_MARCH_VOTE 1
-#endif
+// the rare exact recomputation (SLOW) of an out-of-range lane, by the whole warp when any lane needs it (a
+// warp vote and a uniform branch; SLOW gives the same bits).  The vote also closes the scheduling region there.
 #if !SWOF_EXACT
-// the tolerance build has no slow path, but keeps the warp vote (on a predicate that is never true): it closes
-// the scheduling region there -- one unbroken row body measured 11 % slower (ptxas interleaves the whole row
-// and runs short of registers at 168)
+// the tolerance build has no slow path, but keeps the warp vote (on a predicate that is never true): one
+// unbroken row body measured 11 % slower (ptxas interleaves the whole row and runs short of registers at 168)
 #define M_SLOW(...) ((void)(__VA_ARGS__), __any_sync(0xffffffffu, m_never))
-#elif SWOF_MARCH_VOTE
-#define M_SLOW(...) __any_sync(0xffffffffu, (__VA_ARGS__))
 #else
-#define M_SLOW(...) (__VA_ARGS__)
+#define M_SLOW(...) __any_sync(0xffffffffu, (__VA_ARGS__))
 #endif
 #ifndef SWOF_MARCH_EARLY
 #define SWOF_MARCH_EARLY 1             // interior warps load their first rows before the preamble (+0.75 %)
-#endif
-#ifndef SWOF_MARCH_SCV
-#define SWOF_MARCH_SCV 0
 #endif
 #ifndef SWOF_MARCH_NW
 #define SWOF_MARCH_NW 1                // warps per CTA: 1 -- a CTA retires with its warp (+6.7 % against 4)
@@ -231,11 +218,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
     }
     __syncthreads();
     if (s_done) return;
-#if SWOF_MARCH_SCV    // re-read the step scalars from shared memory at each use (register pressure experiment)
-    const volatile double &dt = s_sc[0], &lx = s_sc[2], &ly = s_sc[3], &Rdt = s_sc[4], &dtgcf0 = s_sc[5];
-#else
     const double dt = s_sc[0], lx = s_sc[2], ly = s_sc[3], Rdt = s_sc[4], dtgcf0 = s_sc[5];
-#endif
     const int nx = P.nx, ny = P.ny, pitch = P.pitch;
     const int nstrip = (nx + M_OWN - 1) / M_OWN;
     const int wid = blockIdx.x * M_NW + warp;
@@ -481,7 +464,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         };
         row(j0, std::false_type{}, std::false_type{});
         row(j0 + 1, std::true_type{}, std::false_type{});
-_Pragma(SWOF_STR(unroll SWOF_MARCH_UNROLL))
+#pragma unroll 1
         for (int j = j0 + 2; j <= jend + 1; ++j) row(j, std::true_type{}, std::true_type{});
         if (__any_sync(0xffffffffu, ncl != 0u) && ncl != 0u) {   // rare: a clamp in this warp's segment
             atomicAdd(&st->clamps, (unsigned long long)ncl);

@@ -54,7 +54,7 @@ for name, kw, steps in CASES:
         peaks, src = bench.load_peaks()
         bp, bc = bench.bytes_per_cell_update(cfg.ga is not None, cfg.fric_field is not None)
         crop = min(256, cfg.nx, cfg.ny)
-        _, cnt, _, nst = bench.cpu_sample(cfg, crop, 4)
+        _, cnt, _, nst, _ = bench.cpu_sample(cfg, crop, 4)
         f_alg = bench.f_alg_from_counters(cnt, cfg, nst, crop * crop)
         peak_gops = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
         roof = {"bytes_per_cell_update": bp + bc, "hbm_frac": (bp + bc) * rate / 1e9 / peaks["hbm_gbs"],
