@@ -21,3 +21,25 @@ def test_omp_build_bitwise(name, nx, ny, steps):
     if cfg.ga is not None:
         assert np.array_equal(a["v"], b["v"])
     assert a["counters"].clamps == b["counters"].clamps and a["counters"].face_mid == b["counters"].face_mid
+
+
+def test_chunked_digest_run_equals_one_run(tmp_path):
+    """tools/oracle_digests.py's resumable chunked run (used for the full-size digests that outlast one GPU-box
+    call) gives the one-call run's state and dt sequence bit for bit, for a step-count and a t_end horizon."""
+    import sys
+    import time
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
+    import oracle_digests as od
+    for name, kw, t_end in (("cfg3", dict(nx=90, ny=64, steps=70), None), ("cfg2", dict(nx=61, ny=47), 40.0)):
+        cfg = make(name, **kw)
+        if t_end is not None:
+            cfg.t_end = t_end
+        a = oracle.run(cfg, omp=True)
+        r, _ = od.run_chunked(cfg, name, tmp_path, 0.0, time.time(), chunk=20)
+        assert r is None                              # checkpointed after the first chunk
+        while r is None:
+            r, _ = od.run_chunked(cfg, name, tmp_path, 0.0, time.time(), chunk=20)
+        for k in ("h", "hu", "hv", "dt"):
+            assert np.array_equal(a[k], r[k]), (name, k)
+        assert a["t"] == r["t"] and a["steps"] == r["steps"]
