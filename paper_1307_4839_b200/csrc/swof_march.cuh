@@ -11,7 +11,8 @@
 
 namespace swof {
 
-constexpr int M_OWN = 28;              // own columns per warp
+constexpr int M_HL = 2;                       // x-halo lanes per side (= the reconstruction radius)
+constexpr int M_OWN = 32 - 2 * M_HL;          // own columns per warp
 // the rare exact recomputation (SLOW) of an out-of-range lane, by the whole warp when any lane needs it (a
 // warp vote and a uniform branch; SLOW gives the same bits).  The vote also closes the scheduling region there.
 #if !SWOF_EXACT
@@ -162,9 +163,9 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         int j00, jend0;
         march_seg(P, wid0 / nstrip0, j00, jend0);
         const int i00 = (wid0 % nstrip0) * M_OWN;
-        early = i00 - HALO >= 0 && i00 - HALO + 32 <= P.nx && j00 >= 2 && j00 < P.ny;
+        early = i00 - M_HL >= 0 && i00 - M_HL + 32 <= P.nx && j00 >= 2 && j00 < P.ny;
         if (early) {
-            size_t o = (size_t)(j00 - 2) * P.pitch + (i00 - HALO + lane);
+            size_t o = (size_t)(j00 - 2) * P.pitch + (i00 - M_HL + lane);
 #pragma unroll
             for (int r = 0; r < 3; ++r, o += P.pitch) {
                 ew[4 * r] = e_h[o];
@@ -235,9 +236,9 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         const bool rus = ph_rusanov<PH>(P);              // Rusanov flux (generic instance only)
         const bool ord1 = ph_order1<PH>(P);              // first order: every slope is 0
         const double2 z2 = make_double2(0.0, 0.0);
-        const int gi = i0 - HALO + lane;
-        const bool own_col = lane >= HALO && lane < HALO + M_OWN && gi < nx;
-        const bool fastx = i0 - HALO >= 0 && i0 - HALO + 32 <= nx;   // all 32 columns inside (warp-uniform)
+        const int gi = i0 - M_HL + lane;
+        const bool own_col = lane >= M_HL && lane < M_HL + M_OWN && gi < nx;
+        const bool fastx = i0 - M_HL >= 0 && i0 - M_HL + 32 <= nx;   // all 32 columns inside (warp-uniform)
 #if SWOF_MARCH_TMA
         // TMA ring: rows j0+1 .. jend+2 (the fetched rows) in chunks of TMA_ROWS, two stages; only for warps whose
         // fetched rows are all stored rows (interior strips, not the last segment: its ghosts are synthesised)
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
                 mbar_expect_tx(bar, 4u * TMA_ROWS * 32 * 8);
                 const int y = j0 + 1 + c * TMA_ROWS + GHOST_ROWS;          // tensor rows start at field row -2
 #pragma unroll
-                for (int f = 0; f < 4; ++f) tma_load_2d(&s_ring[c & 1][f][0][0], tm + f * 128, i0 - HALO, y, bar);
+                for (int f = 0; f < 4; ++f) tma_load_2d(&s_ring[c & 1][f][0][0], tm + f * 128, i0 - M_HL, y, bar);
             }
         };
         if (tma) {
@@ -386,8 +387,8 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
                     double Fcx = 0.0;
                     if (!(DRY && dA)) {                       // a dry row: every x face is dry-dry
                         const double2 heA = make_double2(A.h, A.e);
-                        const double2 cL = shup2(heA), cR = shdn2(heA);
                         const double2 uvA = make_double2(A.u, A.v);
+                        const double2 cL = shup2(heA), cR = shdn2(heA);
                         const double2 uL = shup2(uvA), uR = shdn2(uvA);
                         const double2 sa = ord1 ? z2 : half_slopes(cL.x, A.h, cR.x, cL.y, A.e, cR.y);
                         const double2 sb = ord1 ? z2 : half_slopes(uL.x, A.u, uR.x, uL.y, A.v, uR.y);
