@@ -93,3 +93,14 @@ def test_product_does_not_import_oracle():
         assert "oracle" not in re.sub(r"#.*", "", f.read_text()).replace("never imports the oracle", ""), f
     for f in (ROOT / "paper_1307_4839_b200" / "csrc").iterdir():
         assert "swof_oracle" not in f.read_text(), f
+
+
+def test_c_example_compiles_against_the_header(tmp_path):
+    """examples/lake_and_dam.c (the C ABI from plain C) compiles and links against include/swof.h and
+    libswof.so on a machine without a GPU (it is run by tests/test_gpu_c_example.py)."""
+    import subprocess
+    from paper_1307_4839_b200 import build
+    lib = build.build()
+    subprocess.run(["gcc", "-O2", "-std=c11", "-Wall", "-Werror", "-I", str(ROOT / "include"),
+                    str(ROOT / "examples" / "lake_and_dam.c"), "-L", str(lib.parent), "-lswof", "-lm",
+                    "-o", str(tmp_path / "lake_and_dam")], check=True)
