@@ -45,7 +45,7 @@ lo, hi = best
 cuts = [k for k in range(lo, hi + 1) if "VOTE.ANY" in rows[k][1]]
 bounds = [lo] + [c + 1 for c in cuts] + [hi + 1]
 names = ["fetch + primitives + y stencil + y face", "x stencil + x face", "update + sources"]
-names += (["Heun + CFL speeds", "stores + loop control"] if len(cuts) >= 4 else ["stores + loop control"])
+names += (["Heun + CFL speeds", "after the last vote (stores, loop control, what ptxas placed there)"] if len(cuts) >= 4 else ["after the last vote (stores, loop control, what ptxas placed there)"])
 names += [f"region {i}" for i in range(len(names), 20)]
 print(f"== {kregex}: loop {hex(rows[lo][0])}-{hex(rows[hi][0])}, {len(cuts)} votes")
 for i in range(len(bounds) - 1):
