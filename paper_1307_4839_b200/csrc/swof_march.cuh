@@ -11,9 +11,6 @@
 
 namespace swof {
 
-#ifndef SWOF_XFIRST
-#define SWOF_XFIRST 0
-#endif
 constexpr int M_HL = 2;                       // x-halo lanes per side (= the reconstruction radius)
 constexpr int M_OWN = 32 - 2 * M_HL;          // own columns per warp
 // the rare exact recomputation (SLOW) of an out-of-range lane, by the whole warp when any lane needs it (a
@@ -368,8 +365,8 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
             // DRY: warp rows whose 32 cells all hold h = 0 (carried: dA, dB of rows j-2, j-1; dC of row j)
             const bool dC = DRY && __all_sync(0xffffffffu, C.h == 0.0);
             // x direction of row f = j-2 (window A) by shuffles: slopes, reconstruction, the west face of every
-            // lane (the east face is the next lane's west face) and the centred source; where it sits in the
-            // row body is SWOF_XFIRST (0: after the y face, 1: before it, 2: before the y slopes)
+            // lane (the east face is the next lane's west face) and the centred source; it runs after the y face
+            // (before it: -2.1 %, before the y slopes: -1.2 %)
             double2 wa = z2, wb = z2, ea = z2, eb = z2;       // west / east face of this lane's cell
             double Fcx = 0.0;
             auto xpart = [&]() {
@@ -395,9 +392,6 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
                         Fcx = centred_source(g2, A.h, A.e, sa.x, sa.y);
                     }
             };
-#if SWOF_XFIRST == 2
-            if (FIN) xpart();
-#endif
             // y slopes and y reconstruction of row m = j-1 (normal v, transverse u); not needed when rows
             // j-2..j are dry (both of row j-1's faces are dry-dry, its Fc_y multiplies a zero depth)
             double2 saB = z2, sbB = z2;
@@ -408,9 +402,6 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
                 minusB = recon_minus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
                 plusB = recon_plus(make_double2(Bw.h, Bw.e), Bw.v, Bw.u, Bw.rh, saB, sbB);
             }
-#if SWOF_XFIRST == 1
-            if (FIN) xpart();
-#endif
             if (FACE) {
                 // y face between rows j-2 and j-1: the north face of row j-2, the south face of row j-1
                 double2 nfa = z2, nfb = z2;
@@ -420,9 +411,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
                 }
                 if (FIN) {
                     // ---- finalise row f = j-2 (window A): x direction by shuffles, update, sources ----
-#if SWOF_XFIRST == 0
                     xpart();
-#endif
                     const double pxm = lx * (ea.x - wa.x);
                     const double qx = lx * ((ea.y - wb.x) - Fcx), qy = lx * (eb.y - wb.y);
                     // y half with the south (carried) and north (just computed) faces
