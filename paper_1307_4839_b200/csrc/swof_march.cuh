@@ -276,6 +276,41 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
             m.v = hv * rh;
             m.rh = rh;
         };
+        // the point-wise tail of a finalised cell (f, gc) at offset o (ok: an own cell): rain, Green-Ampt and
+        // friction (cell_sources), the corrector's Heun average and CFL speeds, the stores
+        auto tail_cell = [&](const bool ok, const int f, const int gc, const size_t o, const double h1, const double hu1,
+                             const double hv1, const double u2, const double rhs, const double V, const double cf,
+                             const double Ah0, const double Ahu0, const double Ahv0, const double VA0) {
+            double hst, hu2, hv2, Vn;
+            if (M_SLOW(cell_sources<PH, false>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, rhs, u2, hst, hu2, hv2, Vn)))
+                cell_sources<PH, true>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, rhs, u2, hst, hu2, hv2, Vn);
+            // the values this lane stores: U* (predictor) or the Heun average U^{n+1} (corrector), and the
+            // corrector's CFL speeds, all formed before the store branch (so the speeds' rcp / sqrt chains overlap
+            // the rest of the cell)
+            double oh = hst, ohu = hu2, ohv = hv2, oV = Vn;
+            if (CORRECTOR) {
+                oh = 0.5 * (Ah0 + hst);
+                ohu = 0.5 * (Ahu0 + hu2);
+                ohv = 0.5 * (Ahv0 + hv2);
+                oV = 0.5 * (VA0 + Vn);
+                if (P.cfl_mode == 0) {
+                    double su, sv;
+                    if (M_SLOW(cfl_speeds<false>(P, oh, ohu, ohv, su, sv))) cfl_speeds<true>(P, oh, ohu, ohv, su, sv);
+                    amx = (ok && (su > amx || su != su)) ? su : amx;
+                    amy = (ok && (sv > amy || sv != sv)) ? sv : amy;
+                }
+            }
+            if (ok) {
+                double* const oA = CORRECTOR ? B.Ah : B.Bh;
+                double* const oAu = CORRECTOR ? B.Ahu : B.Bhu;
+                double* const oAv = CORRECTOR ? B.Ahv : B.Bhv;
+                oA[o] = oh;
+                oAu[o] = ohu;
+                oAv[o] = ohv;
+                if (ph_ga<PH>(P)) (CORRECTOR ? B.VA : B.VB)[o] = oV;
+                if (PUSH && (f < GHOST_ROWS || f >= ny - GHOST_ROWS)) push_halo(B, CORRECTOR ? 0 : 1, ny, pitch, f, gc, oh, ohu, ohv);
+            }
+        };
         // window: A = row j-2, Bw = row j-1, C = row j
         MPrim A, Bw, C;
         double rh_, rhu, rhv, rz;                     // raw (h, hu, hv, z) of row j, fetched one row ahead
@@ -424,39 +459,12 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
                     const double hv1 = hvs - (qy + ly * Dn);
                     const double cl = (own && hh < 0.0) ? -hh : 0.0;
                     const double h1 = hh < 0.0 ? 0.0 : hh;
-                    double hst, hu2, hv2, Vn;
-                    if (M_SLOW(cell_sources<PH, false>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn)))
-                        cell_sources<PH, true>(P, dt, dtgcf0, Rdt, h1, hu1, hv1, V, cf, A.rh, hus, hvs, hst, hu2, hv2, Vn);
+                    const double u2 = ph_fk<PH>(P) != 0 ? hus * hus + hvs * hvs : 0.0;
                     ncl += cl > 0.0 ? 1u : 0u;
                     clm += cl;
                     clf = cl > clx ? f : clf;
                     clx = cl > clx ? cl : clx;
-                    // the values this lane stores: U* (predictor) or the Heun average U^{n+1} (corrector), and
-                    // the corrector's CFL speeds, all formed before the own-lane store branch (so the loads of
-                    // U^n stay early and the speeds' rcp / sqrt chains overlap the rest of the row)
-                    double oh = hst, ohu = hu2, ohv = hv2, oV = Vn;
-                    if (CORRECTOR) {
-                        oh = 0.5 * (Ah0 + hst);
-                        ohu = 0.5 * (Ahu0 + hu2);
-                        ohv = 0.5 * (Ahv0 + hv2);
-                        oV = 0.5 * (VA0 + Vn);
-                        if (P.cfl_mode == 0) {
-                            double su, sv;
-                            if (M_SLOW(cfl_speeds<false>(P, oh, ohu, ohv, su, sv))) cfl_speeds<true>(P, oh, ohu, ohv, su, sv);
-                            amx = (own && (su > amx || su != su)) ? su : amx;
-                            amy = (own && (sv > amy || sv != sv)) ? sv : amy;
-                        }
-                    }
-                    if (own) {
-                        double* const oA = CORRECTOR ? B.Ah : B.Bh;
-                        double* const oAu = CORRECTOR ? B.Ahu : B.Bhu;
-                        double* const oAv = CORRECTOR ? B.Ahv : B.Bhv;
-                        oA[o] = oh;
-                        oAu[o] = ohu;
-                        oAv[o] = ohv;
-                        if (ph_ga<PH>(P)) (CORRECTOR ? B.VA : B.VB)[o] = oV;
-                        if (PUSH && (f < GHOST_ROWS || f >= ny - GHOST_ROWS)) push_halo(B, CORRECTOR ? 0 : 1, ny, pitch, f, gi, oh, ohu, ohv);
-                    }
+                    tail_cell(own, f, gi, o, h1, hu1, hv1, u2, A.rh, V, cf, Ah0, Ahu0, Ahv0, VA0);
                 }
                 sfa = make_double2(nfa.x, nfa.y);              // becomes the south face of row j-1
                 sfb = nfb;
