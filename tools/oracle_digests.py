@@ -12,6 +12,7 @@ the same inputs and compares digests: equal digests mean the GPU state equals th
 (hence within every north_star tolerance, masks and dt sequence included).
 
     OMP_NUM_THREADS=7 python tools/oracle_digests.py cfg1 cfg2 cfg4 cfg3
+    OMP_NUM_THREADS=7 python tools/oracle_digests.py cfg4@100 cfg3@500     # full size, the first N steps
     python tools/oracle_digests.py cfg3 --ckpt /tmp/swof_ckpt --max-seconds 3000   # resumable, in chunks
 
 With --ckpt the run advances in chunks of 50 steps and, when --max-seconds is spent, saves the state (h, hu, hv,
@@ -41,6 +42,17 @@ from workloads import make  # noqa: E402
 OUT = ROOT / "tests" / "golden" / "full_size_digests.json"
 NPZ = ROOT / "tests" / "golden" / "full_size"
 N_SAMPLES = 4096
+
+
+def make_named(name: str):
+    """'cfgK' = configuration K at full size over its whole horizon; 'cfgK@N' = the same full-size inputs
+    over the first N steps only (a step-count configuration's prefix: cfg3, cfg4)."""
+    base, _, n = name.partition("@")
+    cfg = make(base)
+    if n:
+        assert cfg.steps is not None and cfg.t_end is None, f"{base} is not a step-count configuration"
+        cfg.steps = int(n)
+    return cfg
 
 
 def sample_index(name: str, ncell: int) -> np.ndarray:
@@ -111,7 +123,7 @@ def main(names, ckpt=None, max_seconds=float("inf")):
                        "configuration's full size and full step count; SHA-256 of the float64 rasters")
     src = source_digest()
     for name in names:
-        cfg = make(name)
+        cfg = make_named(name)
         t0 = time.time()
         if ckpt is None:
             r = oracle.run(cfg, omp=True)
