@@ -107,6 +107,8 @@ def run_chunked(cfg, name, ckpt, max_seconds, t0, chunk=50):
         cmax = max(cmax, float(r["counters"].clamp_max))
         if r["steps"] == 0:
             break
+        if len(dts) % 500 == 0:
+            print(f"{name}: {len(dts)} steps, t = {t:.6g}, {spent + time.time() - t0:.0f} s", file=sys.stderr, flush=True)
         if time.time() - t0 > max_seconds and len(dts) < total and t < t_end:
             Path(ckpt).mkdir(parents=True, exist_ok=True)
             np.savez(path, h=h, hu=hu, hv=hv, v=(v if v is not None else np.zeros(0)), t=t, dt=np.array(dts),
