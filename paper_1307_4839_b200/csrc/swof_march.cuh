@@ -22,12 +22,6 @@ constexpr int M_OWN = 32 - 2 * M_HL;          // own columns per warp
 #else
 #define M_SLOW(...) __any_sync(0xffffffffu, (__VA_ARGS__))
 #endif
-#ifndef SWOF_AMAX_INT
-#define SWOF_AMAX_INT 0                // 1: the corrector's running CFL maxima compared as u64 bit patterns
-#endif
-#ifndef SWOF_CLAMP_ATOMIC
-#define SWOF_CLAMP_ATOMIC 0            // 1: clamps reported by atomics in a rare warp-uniform branch (no per-lane bookkeeping)
-#endif
 #ifndef SWOF_MARCH_EARLY
 #define SWOF_MARCH_EARLY 1             // interior warps load their first rows before the preamble (+0.75 %)
 #endif
@@ -302,15 +296,11 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
                 if (P.cfl_mode == 0) {
                     double su, sv;
                     if (M_SLOW(cfl_speeds<false>(P, oh, ohu, ohv, su, sv))) cfl_speeds<true>(P, oh, ohu, ohv, su, sv);
-#if SWOF_AMAX_INT
                     // su, sv are +0, positive or NaN (never -0): their bit patterns order like their values and a
-                    // NaN's lies above every number's, as in the u64 reduction below (integer pipe, no DSETP)
+                    // NaN's lies above every number's, as in the u64 reduction below, so the running maxima compare
+                    // on the integer pipe (no DSETP; +0.2 % against the fp64 compare with a NaN test)
                     amx = (ok && d2u(su) > d2u(amx)) ? su : amx;
                     amy = (ok && d2u(sv) > d2u(amy)) ? sv : amy;
-#else
-                    amx = (ok && (su > amx || su != su)) ? su : amx;
-                    amy = (ok && (sv > amy || sv != sv)) ? sv : amy;
-#endif
                 }
             }
             if (ok) {
@@ -473,23 +463,10 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
                     const double cl = (own && hh < 0.0) ? -hh : 0.0;
                     const double h1 = hh < 0.0 ? 0.0 : hh;
                     const double u2 = ph_fk<PH>(P) != 0 ? hus * hus + hvs * hvs : 0.0;
-#if SWOF_CLAMP_ATOMIC
-                    // a clamp is rare: the lanes that clamped report it at once (a warp-uniform branch)
-                    if (__any_sync(0xffffffffu, cl > 0.0) && cl > 0.0) {
-                        atomicAdd(&st->clamps, 1ull);
-                        atomicAdd(&st->clamped_mass, cl);
-                        if (atomicMax(&st->clamp_max_bits, d2u(cl)) < d2u(cl)) {
-                            atomicExch((unsigned long long*)&st->big_clamp_cell, (unsigned long long)((long long)f * nx + gi));
-                            atomicExch((unsigned long long*)&st->big_clamp_step, (unsigned long long)st->step[par]);
-                        }
-                        if (cl > P.clamp_fail) atomicOr(&st->flags, FLAG_BIGCLAMP);
-                    }
-#else
                     ncl += cl > 0.0 ? 1u : 0u;
                     clm += cl;
                     clf = cl > clx ? f : clf;
                     clx = cl > clx ? cl : clx;
-#endif
                     tail_cell(own, f, gi, o, h1, hu1, hv1, u2, A.rh, V, cf, Ah0, Ahu0, Ahv0, VA0);
                 }
                 sfa = make_double2(nfa.x, nfa.y);              // becomes the south face of row j-1
@@ -507,7 +484,7 @@ __global__ void __launch_bounds__(M_NW * 32, SWOF_MARCH_MINB) march_kernel(const
         row(j0 + 1, std::true_type{}, std::false_type{});
 #pragma unroll 1
         for (int j = j0 + 2; j <= jend + 1; ++j) row(j, std::true_type{}, std::true_type{});
-        if (!SWOF_CLAMP_ATOMIC && __any_sync(0xffffffffu, ncl != 0u) && ncl != 0u) {   // rare: a clamp in this warp's segment
+        if (__any_sync(0xffffffffu, ncl != 0u) && ncl != 0u) {   // rare: a clamp in this warp's segment
             atomicAdd(&st->clamps, (unsigned long long)ncl);
             atomicAdd(&st->clamped_mass, clm);
             if (atomicMax(&st->clamp_max_bits, d2u(clx)) < d2u(clx)) {
