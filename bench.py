@@ -203,7 +203,7 @@ def fp64_issue_ceiling(peak_gops):
             return None
         return {"value": peak_gops * 1e9 / (32 * per_cell), "unit": UNIT,
                 "fp64_lane_instr_per_cell_update": 32 * per_cell,
-                "source": f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"}
+                "source": f"profiles/ncu_latest.json: {prof['report']}"}
     except Exception:
         return None
 
@@ -228,7 +228,7 @@ def roofline(peaks, src, peak_gops, f_alg, dom, dom_ms, dom_bytes, cells, value,
             is_corr = re.search(r"(stage|march)_kernel<(\(bool\))?(1|true)\b", kname) is not None
             if is_corr == (dom == "corrector"):
                 traffic = k["dram_bytes_per_cell"] * cells
-                tsrc = f"profiles/ncu_latest.json ({os.path.basename(prof['report'])})"
+                tsrc = f"profiles/ncu_latest.json: {prof['report']}"
                 ncu = {"fp64_pipe_pct": k.get("fp64_pipe_pct"), "issue_active_pct": k.get("issue_active_pct"),
                        "dram_throughput_pct": k.get("dram_throughput_pct"), "registers": k.get("registers"),
                        "warps_active_pct": k.get("warps_active_pct")}
