@@ -61,7 +61,7 @@ def _make(name):
     return cfg
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg3@500", "cfg3@2000", "cfg4@100", "cfg4@300"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg3@500", "cfg3@1000", "cfg3@2000", "cfg4@100", "cfg4@300"])
 def test_full_size_full_count(gpu, name):
     ent, ref = _entry(name)
     cfg = _make(name)
